@@ -1,0 +1,150 @@
+/*
+ * esi.h -- C ABI of the B200-native ESI library (libesi.so).
+ *
+ * ESI = Event-based Single Integration, arXiv 2508.02238.  The library turns
+ * an asynchronous event stream e = {x, y, t, p} (Sec. III-A)
+ * into 8-bit intensity frames at caller-chosen frame times (typically 100 FPS,
+ * P:20).  Per event it runs Algorithm 2: add p*C,
+ * decay by Eq. 4 d(dt) = max{(1 - k dt)^b, 0}, set T,
+ * clamp by Eq. 13.  Each frame is the Eq. 14 linear map
+ * B = 255 (S - S_min)/(S_max - S_min) of the state.
+ * The readings of the paper this library implements are listed in DESIGN.md
+ * section 3 (A1..A17); the same readings are used by the fp64 oracle under
+ * oracle/ (which shares no code with this library).
+ *
+ * Threading: one writer per handle.  All GPU work of a
+ * handle runs on its stream (its own, or the one set by esi_set_stream).
+ *
+ * Errors: every call returns an esi_status (0 = ESI_OK).  Invalid events are
+ * detected on the device while they are integrated (fused into the ingest
+ * kernel, so no extra pass over the events).  Such an error is STICKY: the
+ * render call that found it returns it, the frames and state it produced are
+ * unspecified, and every later call returns it until esi_reset().  With
+ * params.validate_on_push = 1, esi_push_events instead validates the batch
+ * eagerly (one extra read of the batch) and rejects it atomically: on error
+ * none of its events is kept and the handle stays usable.  CUDA failures
+ * latch ESI_ERR_CUDA (sticky, also cleared only by esi_reset).
+ */
+#ifndef ESI_H
+#define ESI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESI_ABI_VERSION 1
+
+/* Status codes (numbering of SURVEY.md section 8(b)). */
+typedef enum {
+  ESI_OK = 0,
+  ESI_ERR_INVALID_ARG = 1,       /* null pointer, bad size, bad parameter, frames out of order */
+  ESI_ERR_OUT_OF_BOUNDS = 2,     /* event x >= width or y >= height */
+  ESI_ERR_BAD_POLARITY = 3,      /* event p not in {+1, -1} */
+  ESI_ERR_NEGATIVE_INTERVAL = 4, /* event t below its predecessor, below t_origin, or not later
+                                    than the last rendered frame; frame time going backwards */
+  ESI_ERR_CUDA = 5,              /* any CUDA error (sticky) */
+  ESI_ERR_OOM = 6                /* device or host allocation failure */
+} esi_status;
+
+/* One event, 16 bytes, little-endian; the record layout of SPEC S:370
+ * (t: int64 microseconds, x, y: pixel column/row, p: +1 or -1). */
+typedef struct {
+  int64_t t_us;
+  uint16_t x;
+  uint16_t y;
+  int8_t p;
+  uint8_t _pad[3];
+} esi_event_t;
+
+/* Algorithm 2 inputs and the Eq. 13 bounds. */
+typedef struct {
+  double C;              /* contrast step per event, > 0 (Alg. 2 "C")             */
+  double k;              /* Eq. 4 decay rate in 1/s, > 0                           */
+  double b;              /* Eq. 4 exponent, > 0                                    */
+  double s_min, s_max;   /* Eq. 13 clamp bounds, s_min < s_max                    */
+  int64_t t_origin_us;   /* initial T of every pixel (Alg. 2 "T <- 0", P:239 => default 0) */
+  int32_t readout_decay; /* 1: frame value S*d(t_frame - T), non-mutating (reading A4);
+                            0: Alg. 2 literal, frame maps the stored S             */
+  int32_t device;        /* CUDA device ordinal                                            */
+  int32_t validate_on_push; /* 1: eager, atomic validation in esi_push_events (see above) */
+  int32_t chunk_events;  /* events per pipeline chunk; 0 = default (4 Mi)                  */
+} esi_params_t;
+
+typedef struct esi_handle esi_handle_t;
+
+/* Fills *p with the defaults: C=0.15, k=10, b=2, s_min=-1.5, s_max=1.5 (SPEC S:134,
+ * S:210-211), t_origin 0, readout_decay 1, device 0, lazy validation. */
+void esi_default_params(esi_params_t* p);
+
+/* Creates a handle for a width x height sensor (1 <= width, height <= 65535,
+ * width*height <= 2^23).  Allocates the per-pixel state S (fp32) and T (int64)
+ * on the device, S = 0, T = t_origin (Alg. 2 "Initialize").
+ * Returns ESI_ERR_INVALID_ARG for bad sizes/params, ESI_ERR_OOM, ESI_ERR_CUDA. */
+int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_handle_t** out);
+
+/* Appends n events (the Alg. 2 input E) to the handle's pending stream.
+ * Events must be globally non-decreasing in t (reading A15) and later than the
+ * last rendered frame.
+ *  - host pointer: the events are copied to device memory (pinned-host sources
+ *    are copied asynchronously on the handle's stream; pageable ones
+ *    synchronously).  The caller may reuse the buffer when the call returns.
+ *  - device pointer: ZERO-COPY.  The library BORROWS the buffer: it reads it
+ *    during later esi_render* calls (stream-ordered on the handle's stream), so
+ *    the caller must keep it alive and unmodified until the render that
+ *    integrates its last event has completed (or until esi_reset/esi_destroy).
+ * The buffer must be 8-byte aligned.  n = 0 is a no-op. */
+int esi_push_events(esi_handle_t* h, const esi_event_t* events, size_t n);
+
+/* Renders one frame at t_frame_us: integrates every pending event with
+ * t <= t_frame_us (ties belong to the frame, reading A6), then writes the
+ * width*height row-major 8-bit frame (index y*width + x) to out, which may be
+ * a host or a device pointer.  Later events stay pending.  Synchronous. */
+int esi_render(esi_handle_t* h, int64_t t_frame_us, uint8_t* out);
+
+/* Renders n frames at the non-decreasing host array t_frames_us[0..n) into
+ * out[n][height][width] (host or device).  Bit-identical to n esi_render
+ * calls.  Events with t > t_frames_us[n-1] stay pending.  Synchronous. */
+int esi_render_many(esi_handle_t* h, const int64_t* t_frames_us, size_t n, uint8_t* out);
+
+/* Copies the state out (host pointers, width*height each; either may be NULL).
+ * Pending events are not integrated by this call. */
+int esi_get_state(esi_handle_t* h, float* S, int64_t* T);
+/* Replaces the state (host pointers) -- checkpoint/resume.  Pending events stay. */
+int esi_set_state(esi_handle_t* h, const float* S, const int64_t* T);
+/* S = 0, T = t_origin, no pending events, no rendered frame, clears sticky errors. */
+int esi_reset(esi_handle_t* h);
+/* Makes the handle issue its work on cudaStream_t stream (NULL: the handle's own). */
+int esi_set_stream(esi_handle_t* h, void* cuda_stream);
+/* Returns the sticky error (synchronises the handle's stream). */
+int esi_get_error(esi_handle_t* h);
+void esi_destroy(esi_handle_t* h);
+const char* esi_strerror(int status);
+
+/* ---- instrumentation (used by bench.py and the parity tests) -------------- */
+
+/* Per-kernel device time accumulated by the handle when timing is enabled
+ * (cudaEvents around each launch, on the handle's stream).  kind:
+ * 0 = ingest/partition, 1 = integrate+readout, 2 = readout-only, 3 = other. */
+int esi_enable_kernel_timing(esi_handle_t* h, int enable);
+int esi_kernel_time(esi_handle_t* h, int kind, double* ms_total, int64_t* launches);
+/* Counters of the last render call: launches of this library's kernels,
+ * events integrated, chunks. */
+int esi_last_render_stats(esi_handle_t* h, int64_t* kernel_launches, int64_t* events,
+                          int64_t* chunks);
+
+/* Debug export of the bit-exact grouping step: runs only the
+ * ingest/partition kernel over the pending events of the first chunk and
+ * copies back, for every band (a run of band_px consecutive pixel ids), the
+ * events routed to it in arrival order, as records {t_us, pixel id, p}.
+ * out_* must hold n_out entries; band_start[nb+1] receives the CSR offsets.
+ * Does not consume events. */
+int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8_t* out_p,
+                        size_t n_out, uint32_t* band_start, int32_t* nb_out, int32_t* band_px_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESI_H */

@@ -1,0 +1,127 @@
+// esi_aux.cu -- small kernels around the two main ones:
+//   K4 esi_readout_kernel : frames straight from the global state (no events)
+//   esi_plan_kernel       : how many chunks start at or before the last frame
+//   esi_consume_kernel    : how many events of a segment were integrated
+//   esi_validate_kernel   : eager validation for params.validate_on_push
+#include "esi_device.cuh"
+
+namespace esi {
+
+// One thread per (frame, group of 8 pixels); Eq. 14 readout of the stored state.
+__global__ void __launch_bounds__(256) esi_readout_kernel(ReadoutArgs a) {
+  const int64_t groups = (a.P + 7) / 8;
+  const int64_t total = groups * a.F;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(g / groups);
+    const int64_t px = (g - (int64_t)j * groups) * 8;
+    const int64_t tj = a.tf[j];
+    const int nq = (int)min((int64_t)8, a.P - px);
+    uint32_t bytes[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float v = 0.f;
+      if (q < nq) {
+        v = a.S[px + q];
+        if (a.mp.readout_decay) v *= esi_decay(tj - a.T[px + q], a.dp);
+      }
+      bytes[q] = esi_map8(v, a.mp);
+    }
+    uint8_t* dst = a.out + (int64_t)j * a.P + px;
+    if (a.vec8 && nq == 8) {
+      st_stream8(dst, bytes[0] | (bytes[1] << 8) | (bytes[2] << 16) | (bytes[3] << 24),
+                 bytes[4] | (bytes[5] << 8) | (bytes[6] << 16) | (bytes[7] << 24));
+    } else {
+      for (int q = 0; q < nq; ++q) dst[q] = (uint8_t)bytes[q];
+    }
+  }
+}
+
+cudaError_t launch_readout(const ReadoutArgs& a, cudaStream_t s) {
+  const int64_t total = ((a.P + 7) / 8) * a.F;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  esi_readout_kernel<<<(int)blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void esi_plan_kernel(const esi_event_t* const* chunk_first, int n_chunks, int64_t t_cap,
+                                int32_t* n_active) {
+  // chunk first-event times are non-decreasing: count those <= t_cap
+  int lo = 0, hi = n_chunks;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (chunk_first[mid]->t_us <= t_cap) lo = mid + 1; else hi = mid;
+  }
+  *n_active = lo;
+}
+
+cudaError_t launch_plan(const esi_event_t* const* chunk_first, int n_chunks, int64_t t_cap,
+                        int32_t* n_active, cudaStream_t s) {
+  esi_plan_kernel<<<1, 1, 0, s>>>(chunk_first, n_chunks, t_cap, n_active);
+  return cudaGetLastError();
+}
+
+__global__ void esi_consume_kernel(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,
+                                   int64_t* last_t) {
+  int64_t lo = 0, hi = n;  // number of events with t <= t_cap
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (seg[mid].t_us <= t_cap) lo = mid + 1; else hi = mid;
+  }
+  *count = lo;
+  if (lo > 0) *last_t = seg[lo - 1].t_us;
+}
+
+cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,
+                           int64_t* last_t, cudaStream_t s) {
+  esi_consume_kernel<<<1, 1, 0, s>>>(seg, n, t_cap, count, last_t);
+  return cudaGetLastError();
+}
+
+__global__ void esi_validate_kernel(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
+                                    int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
+                                    unsigned long long* err) {
+  const int4* evv = reinterpret_cast<const int4*>(ev);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 r = ld_stream16(evv + i);
+    const int64_t t = (int64_t)(((uint64_t)(uint32_t)r.y << 32) | (uint32_t)r.x);
+    const uint32_t x = (uint32_t)r.z & 0xffffu, y = (uint32_t)r.z >> 16;
+    const int p = (int)(int8_t)(r.w & 0xff);
+    const int64_t tp = i > 0 ? ev[i - 1].t_us : *prev_t;
+    int code = 0;
+    if (x >= (uint32_t)W || y >= (uint32_t)H) code = ESI_ERR_OUT_OF_BOUNDS;
+    else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
+    else if (t < t_origin || t < tp || t <= last_frame_t) code = ESI_ERR_NEGATIVE_INTERVAL;
+    if (code) atomicMin(err, ((unsigned long long)i << 8) | (unsigned)code);
+  }
+}
+
+cudaError_t launch_validate(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
+                            int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
+                            unsigned long long* err, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  esi_validate_kernel<<<(int)blocks, 256, 0, s>>>(ev, n, prev_t, t_origin, last_frame_t, W, H, err);
+  return cudaGetLastError();
+}
+
+}  // namespace esi
+
+namespace esi {
+__global__ void esi_fill_i64_kernel(int64_t* p, int64_t n, int64_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+cudaError_t launch_fill_i64(int64_t* p, int64_t n, int64_t v, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  esi_fill_i64_kernel<<<(int)blocks, 256, 0, s>>>(p, n, v);
+  return cudaGetLastError();
+}
+}  // namespace esi

@@ -1,0 +1,68 @@
+// esi_device.cuh -- small device helpers shared by the libesi kernels.
+#pragma once
+#include <cstdint>
+#include "esi_internal.cuh"
+
+namespace esi {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// 16-byte streaming load (read once: evict-first in L1/L2).
+__device__ __forceinline__ int4 ld_stream16(const int4* p) { return __ldcs(p); }
+
+// 8-byte streaming store of frame bytes.
+__device__ __forceinline__ void st_stream8(void* p, uint32_t lo, uint32_t hi) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(lo), "r"(hi) : "memory");
+}
+
+// Eq. 4: d(dt) = max{(1 - k dt)^b, 0}, dt in integer microseconds (>= 0).
+// u = 1 - k dt is formed with a float pair (kh + kl = k * 1e-6) so that u keeps
+// ~1 ulp relative accuracy near the cutoff (SURVEY 8(c) numerics); dt >= dt_cut
+// (= ceil(1e6/k)) gives d = 0 exactly (reading A14).
+__device__ __forceinline__ float esi_decay(int64_t dt, const DecayParams& dp) {
+  if (dt >= dp.dt_cut) return 0.f;
+  float u;
+  if (dp.use_f64) {
+    u = (float)(1.0 - dp.k_us * (double)dt);
+  } else {
+    const float f = (float)(int32_t)dt;  // exact: dt < dt_cut <= 2^24
+    u = fmaf(-f, dp.kh, 1.0f);
+    u = fmaf(-f, dp.kl, u);
+  }
+  u = fmaxf(u, 0.f);
+  switch (dp.bmode) {
+    case 1: return u;
+    case 2: return u * u;
+    case 3: return u * u * u;
+    case 4: { const float u2 = u * u; return u2 * u2; }
+    default: return u > 0.f ? exp2f(dp.b * log2f(u)) : 0.f;
+  }
+}
+
+// Eq. 13 + Eq. 14: clamp, then 255 (v - smin)/(smax - smin)
+// rounded half away from zero (reading A8; q >= 0 here so floor(q + 0.5)),
+// computed as off_int + floor(v*scale + off_frac).
+__device__ __forceinline__ uint32_t esi_map8(float v, const MapParams& mp) {
+  v = fminf(fmaxf(v, mp.smin), mp.smax);
+  int q = mp.off_int + __float2int_rd(fmaf(v, mp.scale, mp.off_frac));
+  q = min(max(q, 0), 255);
+  return (uint32_t)q;
+}
+
+// number of entries of the sorted array a[0..n) that are < key
+__device__ __forceinline__ int lower_bound_i64(const int64_t* a, int n, int64_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace esi

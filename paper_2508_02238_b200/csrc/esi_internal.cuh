@@ -1,0 +1,123 @@
+// esi_internal.cuh -- device-side types and launchers of libesi (sm_100a).
+//
+// Pipeline of one render call:
+//   plan      : which chunks hold events with t <= last frame time        (tiny)
+//   per chunk of <= chunk_events pending events:
+//     K1 esi_partition_kernel : 16-B vector ingest + validation + stable,
+//        bit-exact partition of each 8192-event tile by pixel band
+//     K2 esi_integrate_kernel : one CTA per band; gathers the band's events
+//        in arrival order, applies Alg. 2 per event (per-pixel arrival order
+//        kept by lowest-lane-first rounds) to the band's state in shared
+//        memory, and writes every frame of the chunk (fused Eq. 14 readout)
+//   consume   : how many pending events were integrated                   (tiny)
+//   K4 esi_readout_kernel   : frames when no event is pending (readout only)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/esi.h"
+
+namespace esi {
+
+constexpr int kTile = 8192;          // events per partition CTA
+constexpr int kPartThreads = 512;    // 16 warps x 16 events per thread
+constexpr int kSubBatch = 1024;      // band events staged in smem per sub-batch
+constexpr int kMaxTilesPerChunk = 1024;
+constexpr int kWarpPx = 256;         // pixels owned by one warp (8 per lane)
+constexpr int kMaxBands = 1024;
+constexpr int kMaxBandPx = 4096;
+
+// First error of a render call: (global event index << 8) | code, atomicMin'ed
+// so that the earliest offending event wins (same as the oracle's first error).
+constexpr unsigned long long kNoError = ~0ull;
+
+struct DecayParams {
+  float kh, kl;          // k * 1e-6 split into a float pair (u = 1 - k dt, dt in us)
+  double k_us;           // k * 1e-6 in double (fallback when dt_cut > 2^24)
+  int64_t dt_cut;        // smallest dt (us) with 1 - k dt <= 0: ceil(1e6 / k)
+  int32_t use_f64;
+  int32_t bmode;         // 1,2,3,4: integer b fast path; 0: exp2(b log2 u)
+  float b;
+};
+
+struct MapParams {
+  float C;               // contrast step
+  float smin, smax;      // Eq. 13 bounds
+  // Eq. 14 + 0.5 = v*scale + off, off = -smin*scale + 0.5 split as off_int + off_frac so
+  // that a tiny |v| is not absorbed by the offset (v = -1e-9 must give 127, not 128).
+  float scale, off_frac;
+  int32_t off_int;
+  int32_t readout_decay;
+};
+
+struct PartArgs {
+  const esi_event_t* ev;     // this chunk's events
+  int64_t n;                 // events in the chunk
+  int64_t index_base;        // index of ev[0] among this render's pending events
+  const int64_t* prev_t;     // t of the event preceding ev[0] (device address)
+  int64_t t_origin;
+  int64_t last_frame_t;      // events must be > this (INT64_MIN if no frame yet)
+  int64_t t_cap;             // last frame time of the render call
+  int32_t W, H;
+  int32_t band_shift, nb, nb_bits;
+  uint2* rec;                // [n_tiles * kTile] tile-local band-sorted records
+  uint32_t* meta;            // [nb][n_tiles]: offset | count << 16
+  int64_t* tile_t0;          // [n_tiles]
+  int32_t* tile_wide;        // [n_tiles]
+  int64_t* wide_t;           // [n_tiles * kTile] full t, written for wide tiles only
+  unsigned long long* err;
+};
+
+struct IntArgs {
+  const uint2* rec;
+  const uint32_t* meta;
+  const int64_t* tile_t0;
+  const int32_t* tile_wide;
+  const int64_t* wide_t;
+  int32_t n_tiles;
+  int32_t first_chunk;
+  int64_t n;                         // events in the chunk
+  const esi_event_t* ev;             // chunk events (first/last t)
+  const esi_event_t* ev_next;        // first event of the next chunk or nullptr
+  const int64_t* tf;                 // frame times (device)
+  int32_t F;
+  int64_t t_cap;
+  float* S;
+  int64_t* T;
+  uint8_t* out;                      // [F][P]
+  int64_t P;
+  int32_t band_px, nb;
+  int32_t vec8;                      // 8-byte frame stores allowed
+  DecayParams dp;
+  MapParams mp;
+};
+
+struct ReadoutArgs {
+  const float* S;
+  const int64_t* T;
+  const int64_t* tf;
+  int32_t F;
+  uint8_t* out;
+  int64_t P;
+  int32_t vec8;
+  DecayParams dp;
+  MapParams mp;
+};
+
+size_t partition_smem_bytes(int nb);
+size_t integrate_smem_bytes(int band_px);
+cudaError_t launch_partition(const PartArgs& a, int n_tiles, cudaStream_t s);
+cudaError_t launch_integrate(const IntArgs& a, cudaStream_t s);
+cudaError_t launch_readout(const ReadoutArgs& a, cudaStream_t s);
+// plan: active[c] = 1 if chunk c's first event has t <= t_cap; count into *n_active
+cudaError_t launch_plan(const esi_event_t* const* chunk_first, int n_chunks, int64_t t_cap,
+                        int32_t* n_active, cudaStream_t s);
+// consume: for segment k, count events with t <= t_cap (binary search), and set
+// *last_t to the t of the last consumed event of the last segment with one.
+cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,
+                           int64_t* last_t, cudaStream_t s);
+cudaError_t launch_fill_i64(int64_t* p, int64_t n, int64_t v, cudaStream_t s);
+cudaError_t launch_validate(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
+                            int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
+                            unsigned long long* err, cudaStream_t s);
+
+}  // namespace esi

@@ -1,0 +1,206 @@
+// esi_partition.cu -- K1: event ingest + validation + stable partition by band.
+//
+// One CTA per tile of kTile (8192) consecutive pending events.  Each lane loads
+// one 16-byte esi_event_t per step (a warp reads 512 contiguous bytes), checks
+// it (reading A15: t non-decreasing, >= t_origin, > last frame),
+// and computes its pixel id y*W + x and its band = pid >> band_shift.  The tile
+// is then stably partitioned by band -- band-major, arrival-order-minor, i.e.
+// exactly std::stable_sort by band -- with
+//   * warp multi-split ranks from ballots over the band bits (no atomics, so
+//     the order is deterministic by construction),
+//   * per-warp band histograms in shared memory, a per-band prefix over warps
+//     and a block scan over bands,
+//   * a scatter into a shared-memory copy of the tile and one coalesced
+//     16-byte-vector write of the sorted tile.
+// Record (8 B): x = low 32 bits of t, y = pixel-in-band | (p < 0) << 31.
+// meta[band][tile] = offset-in-tile | count << 16 tells K2 where its events are.
+#include "esi_device.cuh"
+
+namespace esi {
+
+size_t partition_smem_bytes(int nb) {
+  const int nbp = (nb + 1) & ~1;
+  return (size_t)kTile * sizeof(uint2) + (size_t)16 * nbp * sizeof(uint16_t) +
+         (size_t)(nb + 1) * sizeof(uint32_t) + 64 * sizeof(uint32_t);
+}
+
+// Exclusive scan of v[0..n) in place (n <= 2 * kPartThreads); v[n] = total.
+__device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i0 = 2 * tid;
+  const uint32_t a0 = i0 < n ? v[i0] : 0u;
+  const uint32_t a1 = i0 + 1 < n ? v[i0 + 1] : 0u;
+  const uint32_t s = a0 + a1;
+  uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kPartThreads / 32 ? wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    wsum[32 + lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  const uint32_t excl = x - s + (warp ? wsum[32 + warp - 1] : 0u);
+  if (i0 < n) v[i0] = excl;
+  if (i0 + 1 < n) v[i0 + 1] = excl + a0;
+  if (tid == 0) v[n] = wsum[32 + kPartThreads / 32 - 1];
+}
+
+__global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int nbp = (a.nb + 1) & ~1;
+  uint2* sbuf = reinterpret_cast<uint2*>(smem);
+  uint16_t* hist = reinterpret_cast<uint16_t*>(sbuf + kTile);    // [16][nbp]
+  uint32_t* boff = reinterpret_cast<uint32_t*>(hist + 16 * nbp);  // [nb + 1]
+  uint32_t* wsum = boff + a.nb + 1;                               // [64]
+  __shared__ int s_wide;
+
+  // Chunk entirely after the last frame of this render: nothing to integrate.
+  if (a.ev[0].t_us > a.t_cap) return;
+
+  const int tile = blockIdx.x;
+  const int64_t e0 = (int64_t)tile * kTile;
+  const int ne = (int)min((int64_t)kTile, a.n - e0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const esi_event_t* ev = a.ev + e0;
+  const int4* evv = reinterpret_cast<const int4*>(ev);
+  const uint32_t band_mask = (1u << a.band_shift) - 1u;
+
+  for (int i = threadIdx.x; i < 16 * nbp; i += kPartThreads) hist[i] = 0;
+  __syncthreads();
+
+  uint16_t* myhist = hist + warp * nbp;
+  uint2 rec[16];
+  uint32_t rk[16];
+
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    int4 raw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = warp * 512 + (g * 4 + u) * 32 + lane;
+      raw[u] = (i < ne) ? ld_stream16(evv + i) : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = g * 4 + u;
+      const int i = warp * 512 + r * 32 + lane;
+      const bool act = i < ne;
+      const int64_t t = (int64_t)(((uint64_t)(uint32_t)raw[u].y << 32) | (uint32_t)raw[u].x);
+      uint32_t x = (uint32_t)raw[u].z & 0xffffu;
+      uint32_t y = (uint32_t)raw[u].z >> 16;
+      int p = (int)(int8_t)(raw[u].w & 0xff);
+      int64_t tp = __shfl_up_sync(kFull, t, 1);
+      if (lane == 0 && act) tp = (i > 0) ? ev[i - 1].t_us : (tile > 0 ? ev[-1].t_us : *a.prev_t);
+      if (act) {
+        int code = 0;
+        if (x >= (uint32_t)a.W || y >= (uint32_t)a.H) code = ESI_ERR_OUT_OF_BOUNDS;
+        else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
+        else if (t < a.t_origin || t < tp || t <= a.last_frame_t) code = ESI_ERR_NEGATIVE_INTERVAL;
+        if (code) {
+          atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + i) << 8) | (unsigned)code);
+          x = 0; y = 0; p = 1;   // keep the pipeline well-defined; the call reports the error
+        }
+      }
+      const uint32_t pid = y * (uint32_t)a.W + x;
+      const uint32_t band = act ? (pid >> a.band_shift) : 0u;
+      rec[r] = make_uint2((uint32_t)t, (pid & band_mask) | (p < 0 ? 0x80000000u : 0u));
+      // warp multi-split: lanes whose band equals mine
+      unsigned peers = __ballot_sync(kFull, act);
+      for (int bit = 0; bit < a.nb_bits; ++bit) {
+        const bool bset = (band >> bit) & 1u;
+        const unsigned bb = __ballot_sync(kFull, bset);
+        peers &= bset ? bb : ~bb;
+      }
+      if (!act) peers = 0u;
+      const unsigned rank = __popc(peers & lanemask_lt());
+      uint32_t base = 0;
+      if (act && rank == 0) {
+        base = myhist[band];
+        myhist[band] = (uint16_t)(base + __popc(peers));
+      }
+      base = __shfl_sync(kFull, base, act ? (__ffs(peers) - 1) : lane);
+      __syncwarp();
+      rk[r] = (base + rank) | (band << 16);
+    }
+  }
+  __syncthreads();
+
+  // per band: exclusive prefix over the 16 warps, band total into boff[band]
+  for (int b = threadIdx.x; b < a.nb; b += kPartThreads) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) {
+      const uint32_t c = hist[w * nbp + b];
+      hist[w * nbp + b] = (uint16_t)run;
+      run += c;
+    }
+    boff[b] = run;
+  }
+  __syncthreads();
+  part_block_exclusive_scan(boff, a.nb, wsum);
+  __syncthreads();
+
+  for (int b = threadIdx.x; b < a.nb; b += kPartThreads) {
+    const uint32_t cnt = boff[b + 1] - boff[b];
+    a.meta[(int64_t)b * gridDim.x + tile] = boff[b] | (cnt << 16);
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int i = warp * 512 + r * 32 + lane;
+    if (i < ne) {
+      const uint32_t band = rk[r] >> 16;
+      const uint32_t pos = boff[band] + hist[warp * nbp + band] + (rk[r] & 0xffffu);
+      sbuf[pos] = rec[r];
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int64_t t0 = ev[0].t_us, t1 = ev[ne - 1].t_us;
+    a.tile_t0[tile] = t0;
+    s_wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
+    a.tile_wide[tile] = s_wide;
+  }
+  __syncthreads();
+
+  uint4* dst = reinterpret_cast<uint4*>(a.rec + e0);
+  const uint4* src = reinterpret_cast<const uint4*>(sbuf);
+  const int n2 = ne >> 1;
+  for (int i = threadIdx.x; i < n2; i += kPartThreads) dst[i] = src[i];
+  if ((ne & 1) && threadIdx.x == 0) a.rec[e0 + ne - 1] = sbuf[ne - 1];
+
+  if (s_wide) {  // rare: tile spans >= 2^32 us; keep the full timestamps beside the records
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int i = warp * 512 + r * 32 + lane;
+      if (i < ne) {
+        const uint32_t band = rk[r] >> 16;
+        const uint32_t pos = boff[band] + hist[warp * nbp + band] + (rk[r] & 0xffffu);
+        a.wide_t[e0 + pos] = ev[i].t_us;
+      }
+    }
+  }
+}
+
+cudaError_t launch_partition(const PartArgs& a, int n_tiles, cudaStream_t s) {
+  const size_t smem = partition_smem_bytes(a.nb);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  esi_partition_kernel<<<n_tiles, kPartThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace esi

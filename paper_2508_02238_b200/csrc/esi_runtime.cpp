@@ -1,0 +1,710 @@
+// esi_runtime.cpp -- host runtime behind the C ABI of include/esi.h.
+//
+// A handle owns: the device state S (fp32) / T (int64) of Alg. 2,
+// the list of pending event segments (borrowed device buffers or device copies
+// of host pushes), the per-chunk scratch of K1/K2, and a stream.  A render call
+// plans chunks of <= chunk_events pending events (whole segments never mix),
+// runs K1 + K2 per chunk on the stream, then counts the consumed events and
+// reads back the first error -- one small synchronisation per render call.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "esi_internal.cuh"
+
+namespace esi {
+cudaError_t launch_fill_i64(int64_t* p, int64_t n, int64_t v, cudaStream_t s);
+}
+
+using namespace esi;
+
+namespace {
+
+struct Segment {
+  const esi_event_t* ptr;  // first pending event
+  int64_t n;               // pending events
+  void* owned;             // device buffer owned by the handle (host pushes), or nullptr
+  size_t owned_bytes;
+};
+
+struct Chunk {
+  const esi_event_t* ptr;
+  int64_t n;
+  int seg;
+};
+
+struct TimedLaunch {
+  int kind;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct esi_handle {
+  int32_t W = 0, H = 0;
+  int64_t P = 0;
+  esi_params_t prm{};
+  int band_shift = 8, band_px = 256, nb = 1, nb_bits = 0;
+  int64_t chunk_events = 0;
+  int max_tiles = 0;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  float* dS = nullptr;
+  int64_t* dT = nullptr;
+  std::vector<Segment> segs;
+  // K1/K2 scratch
+  uint2* rec = nullptr;
+  uint32_t* meta = nullptr;
+  int64_t* tile_t0 = nullptr;
+  int32_t* tile_wide = nullptr;
+  int64_t* wide_t = nullptr;
+  // small device buffers
+  int64_t* d_tf = nullptr;
+  size_t tf_cap = 0;
+  const esi_event_t** d_chunk_first = nullptr;
+  size_t cf_cap = 0;
+  int64_t* d_cons = nullptr;
+  size_t cons_cap = 0;
+  unsigned long long* d_err = nullptr;
+  int64_t* d_last_t = nullptr;
+  int32_t* d_n_active = nullptr;
+  // pinned host scratch
+  unsigned char* h_pin = nullptr;
+  size_t h_pin_cap = 0;
+  // device frame staging for host outputs
+  uint8_t* d_frames = nullptr;
+  size_t frames_cap = 0;
+  std::vector<std::pair<void*, size_t>> pool;  // free device staging buffers
+  int sticky = ESI_OK;
+  bool has_last_frame = false;
+  int64_t last_frame_t = INT64_MIN;
+  DecayParams dp{};
+  MapParams mp{};
+  bool timing = false;
+  double kt_ms[4] = {0, 0, 0, 0};
+  int64_t kt_n[4] = {0, 0, 0, 0};
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> ev_pool;
+  int64_t st_launches = 0, st_events = 0, st_chunks = 0;
+};
+
+namespace {
+
+int cuda_fail(esi_handle_t* h, cudaError_t e) {
+  if (e == cudaSuccess) return ESI_OK;
+  if (getenv("ESI_DEBUG")) fprintf(stderr, "[esi] CUDA error: %s\n", cudaGetErrorString(e));
+  if (h) h->sticky = ESI_ERR_CUDA;
+  return ESI_ERR_CUDA;
+}
+
+#define ESI_CUDA(h, call)                          \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_); \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int ensure_pinned(esi_handle_t* h, size_t bytes) {
+  if (bytes <= h->h_pin_cap) return ESI_OK;
+  if (h->h_pin) cudaFreeHost(h->h_pin);
+  h->h_pin = nullptr;
+  size_t cap = std::max<size_t>(bytes, 4096);
+  if (cudaMallocHost((void**)&h->h_pin, cap) != cudaSuccess) {
+    cudaGetLastError();
+    h->h_pin_cap = 0;
+    return ESI_ERR_OOM;
+  }
+  h->h_pin_cap = cap;
+  return ESI_OK;
+}
+
+template <typename T>
+int ensure_dev(esi_handle_t* h, T** p, size_t* cap, size_t n) {
+  if (n <= *cap) return ESI_OK;
+  if (*p) cudaFree((void*)*p);
+  *p = nullptr;
+  size_t c = std::max<size_t>(n, 64);
+  if (cudaMalloc((void**)p, c * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();
+    *cap = 0;
+    return ESI_ERR_OOM;
+  }
+  *cap = c;
+  return ESI_OK;
+}
+
+void* pool_take(esi_handle_t* h, size_t bytes, size_t* got) {
+  size_t best = SIZE_MAX;
+  int bi = -1;
+  for (size_t i = 0; i < h->pool.size(); ++i)
+    if (h->pool[i].second >= bytes && h->pool[i].second < best) { best = h->pool[i].second; bi = (int)i; }
+  if (bi >= 0) {
+    void* p = h->pool[bi].first;
+    *got = h->pool[bi].second;
+    h->pool.erase(h->pool.begin() + bi);
+    return p;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  *got = bytes;
+  return p;
+}
+
+void pool_give(esi_handle_t* h, void* p, size_t bytes) {
+  if (p) h->pool.push_back({p, bytes});
+}
+
+void drop_segments(esi_handle_t* h) {
+  for (auto& s : h->segs) pool_give(h, s.owned, s.owned_bytes);
+  h->segs.clear();
+}
+
+cudaEvent_t take_event(esi_handle_t* h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void timed_begin(esi_handle_t* h, int kind, TimedLaunch* tl) {
+  if (!h->timing) return;
+  tl->kind = kind;
+  tl->a = take_event(h);
+  tl->b = take_event(h);
+  cudaEventRecord(tl->a, h->stream);
+}
+
+void timed_end(esi_handle_t* h, TimedLaunch* tl) {
+  if (!h->timing) return;
+  cudaEventRecord(tl->b, h->stream);
+  h->timed.push_back(*tl);
+}
+
+void collect_timing(esi_handle_t* h) {
+  for (auto& tl : h->timed) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, tl.a, tl.b) == cudaSuccess) {
+      h->kt_ms[tl.kind] += ms;
+      h->kt_n[tl.kind] += 1;
+    }
+    cudaGetLastError();
+    h->ev_pool.push_back(tl.a);
+    h->ev_pool.push_back(tl.b);
+  }
+  h->timed.clear();
+}
+
+int params_ok(const esi_params_t* p) {
+  if (!(p->C > 0.0) || !std::isfinite(p->C)) return 0;
+  if (!(p->k > 0.0) || !std::isfinite(p->k)) return 0;
+  if (!(p->b > 0.0) || !std::isfinite(p->b)) return 0;
+  if (!std::isfinite(p->s_min) || !std::isfinite(p->s_max) || !(p->s_min < p->s_max)) return 0;
+  if (p->chunk_events < 0) return 0;
+  return 1;
+}
+
+void derive_params(esi_handle_t* h) {
+  const esi_params_t& p = h->prm;
+  const double kk = p.k * 1e-6;  // 1/us
+  h->dp.kh = (float)kk;
+  h->dp.kl = (float)(kk - (double)h->dp.kh);
+  h->dp.k_us = kk;
+  const double horizon = 1e6 / p.k;  // us
+  h->dp.dt_cut = horizon >= 9.0e18 ? INT64_MAX : (int64_t)std::ceil(horizon);
+  h->dp.use_f64 = h->dp.dt_cut > (int64_t)(1 << 24);
+  h->dp.b = (float)p.b;
+  h->dp.bmode = (p.b == 1.0 || p.b == 2.0 || p.b == 3.0 || p.b == 4.0) ? (int)p.b : 0;
+  h->mp.C = (float)p.C;
+  h->mp.smin = (float)p.s_min;
+  h->mp.smax = (float)p.s_max;
+  const double range = p.s_max - p.s_min;
+  h->mp.scale = (float)(255.0 / range);
+  const double off = -p.s_min * 255.0 / range + 0.5;
+  h->mp.off_int = (int32_t)std::floor(off);
+  h->mp.off_frac = (float)(off - std::floor(off));
+  h->mp.readout_decay = p.readout_decay ? 1 : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+void esi_default_params(esi_params_t* p) {
+  if (!p) return;
+  memset(p, 0, sizeof(*p));
+  p->C = 0.15;
+  p->k = 10.0;
+  p->b = 2.0;
+  p->s_min = -1.5;
+  p->s_max = 1.5;
+  p->t_origin_us = 0;
+  p->readout_decay = 1;
+  p->device = 0;
+  p->validate_on_push = 0;
+  p->chunk_events = 0;
+}
+
+const char* esi_strerror(int s) {
+  switch (s) {
+    case ESI_OK: return "ok";
+    case ESI_ERR_INVALID_ARG: return "invalid argument";
+    case ESI_ERR_OUT_OF_BOUNDS: return "event coordinates outside the sensor";
+    case ESI_ERR_BAD_POLARITY: return "event polarity not +1/-1";
+    case ESI_ERR_NEGATIVE_INTERVAL: return "negative time interval (events or frames out of order)";
+    case ESI_ERR_CUDA: return "CUDA error";
+    case ESI_ERR_OOM: return "out of memory";
+    default: return "unknown status";
+  }
+}
+
+int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_handle_t** out) {
+  if (!out) return ESI_ERR_INVALID_ARG;
+  *out = nullptr;
+  esi_params_t prm;
+  if (params) prm = *params; else esi_default_params(&prm);
+  if (width < 1 || height < 1 || width > 65535 || height > 65535) return ESI_ERR_INVALID_ARG;
+  const int64_t P = (int64_t)width * height;
+  if (P > (int64_t)kMaxBands * kMaxBandPx) return ESI_ERR_INVALID_ARG;
+  if (!params_ok(&prm)) return ESI_ERR_INVALID_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || prm.device < 0 || prm.device >= ndev) {
+    cudaGetLastError();
+    return prm.device < 0 ? ESI_ERR_INVALID_ARG : ESI_ERR_CUDA;
+  }
+  if (cudaSetDevice(prm.device) != cudaSuccess) return ESI_ERR_CUDA;
+
+  esi_handle_t* h = new esi_handle_t();
+  h->W = width;
+  h->H = height;
+  h->P = P;
+  h->prm = prm;
+  derive_params(h);
+  h->band_px = kWarpPx;
+  while ((P + h->band_px - 1) / h->band_px > kMaxBands) h->band_px <<= 1;
+  h->band_shift = 0;
+  while ((1 << h->band_shift) < h->band_px) ++h->band_shift;
+  h->nb = (int)((P + h->band_px - 1) / h->band_px);
+  h->nb_bits = 0;
+  while ((1 << h->nb_bits) < h->nb) ++h->nb_bits;
+  int64_t ce = prm.chunk_events > 0 ? prm.chunk_events : (int64_t)4 << 20;
+  ce = ((ce + kTile - 1) / kTile) * kTile;
+  ce = std::min<int64_t>(ce, (int64_t)kMaxTilesPerChunk * kTile);
+  h->chunk_events = ce;
+  h->max_tiles = (int)(ce / kTile);
+
+  int rc = ESI_OK;
+  auto dalloc = [&](void** p, size_t bytes) {
+    if (rc) return;
+    if (cudaMalloc(p, bytes) != cudaSuccess) { cudaGetLastError(); rc = ESI_ERR_OOM; }
+  };
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) rc = ESI_ERR_CUDA;
+  h->stream = h->own_stream;
+  dalloc((void**)&h->dS, P * sizeof(float));
+  dalloc((void**)&h->dT, P * sizeof(int64_t));
+  dalloc((void**)&h->rec, ce * sizeof(uint2));
+  dalloc((void**)&h->meta, (size_t)h->nb * h->max_tiles * sizeof(uint32_t));
+  dalloc((void**)&h->tile_t0, h->max_tiles * sizeof(int64_t));
+  dalloc((void**)&h->tile_wide, h->max_tiles * sizeof(int32_t));
+  dalloc((void**)&h->wide_t, ce * sizeof(int64_t));
+  dalloc((void**)&h->d_err, sizeof(unsigned long long));
+  dalloc((void**)&h->d_last_t, sizeof(int64_t));
+  dalloc((void**)&h->d_n_active, sizeof(int32_t));
+  if (!rc) rc = ensure_pinned(h, 1 << 16);
+  if (!rc) rc = esi_reset(h);
+  if (!rc && cudaStreamSynchronize(h->stream) != cudaSuccess) rc = ESI_ERR_CUDA;
+  if (rc) {
+    esi_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return ESI_OK;
+}
+
+void esi_destroy(esi_handle_t* h) {
+  if (!h) return;
+  cudaSetDevice(h->prm.device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  drop_segments(h);
+  for (auto& p : h->pool) cudaFree(p.first);
+  for (auto& tl : h->timed) { cudaEventDestroy(tl.a); cudaEventDestroy(tl.b); }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  void* bufs[] = {h->dS, h->dT, h->rec, h->meta, h->tile_t0, h->tile_wide, h->wide_t, h->d_tf,
+                  (void*)h->d_chunk_first, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (h->h_pin) cudaFreeHost(h->h_pin);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  cudaGetLastError();
+  delete h;
+}
+
+int esi_reset(esi_handle_t* h) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  cudaSetDevice(h->prm.device);
+  cudaStreamSynchronize(h->stream);
+  cudaGetLastError();
+  drop_segments(h);
+  h->sticky = ESI_OK;
+  h->has_last_frame = false;
+  h->last_frame_t = INT64_MIN;
+  ESI_CUDA(h, cudaMemsetAsync(h->dS, 0, h->P * sizeof(float), h->stream));
+  ESI_CUDA(h, launch_fill_i64(h->dT, h->P, h->prm.t_origin_us, h->stream));
+  ESI_CUDA(h, launch_fill_i64(h->d_last_t, 1, INT64_MIN, h->stream));
+  return ESI_OK;
+}
+
+int esi_set_stream(esi_handle_t* h, void* s) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  cudaSetDevice(h->prm.device);
+  cudaStreamSynchronize(h->stream);
+  h->stream = s ? (cudaStream_t)s : h->own_stream;
+  return ESI_OK;
+}
+
+int esi_get_error(esi_handle_t* h) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  cudaSetDevice(h->prm.device);
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cuda_fail(h, cudaGetLastError());
+  return h->sticky;
+}
+
+int esi_push_events(esi_handle_t* h, const esi_event_t* events, size_t n) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  if (h->sticky) return h->sticky;
+  if (n == 0) return ESI_OK;
+  if (!events || ((uintptr_t)events & 7)) return ESI_ERR_INVALID_ARG;
+  cudaSetDevice(h->prm.device);
+  Segment sg{events, (int64_t)n, nullptr, 0};
+  if (!is_device_ptr(events)) {
+    size_t got = 0;
+    void* buf = pool_take(h, n * sizeof(esi_event_t), &got);
+    if (!buf) return ESI_ERR_OOM;
+    cudaError_t e = cudaMemcpyAsync(buf, events, n * sizeof(esi_event_t), cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // caller may reuse its buffer
+    if (e != cudaSuccess) {
+      pool_give(h, buf, got);
+      return cuda_fail(h, e);
+    }
+    sg.ptr = (const esi_event_t*)buf;
+    sg.owned = buf;
+    sg.owned_bytes = got;
+  }
+  if (h->prm.validate_on_push) {
+    const int64_t* prev = h->segs.empty() ? h->d_last_t : &h->segs.back().ptr[h->segs.back().n - 1].t_us;
+    ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), h->stream));
+    ESI_CUDA(h, launch_validate(sg.ptr, sg.n, prev, h->prm.t_origin_us,
+                                h->has_last_frame ? h->last_frame_t : INT64_MIN, h->W, h->H, h->d_err,
+                                h->stream));
+    unsigned long long* herr = (unsigned long long*)h->h_pin;
+    ESI_CUDA(h, cudaMemcpyAsync(herr, h->d_err, sizeof(*herr), cudaMemcpyDeviceToHost, h->stream));
+    ESI_CUDA(h, cudaStreamSynchronize(h->stream));
+    if (*herr != kNoError) {
+      pool_give(h, sg.owned, sg.owned_bytes);
+      return (int)(*herr & 0xff);  // atomic rejection; the handle stays usable
+    }
+  }
+  h->segs.push_back(sg);
+  return ESI_OK;
+}
+
+int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  if (h->sticky) return h->sticky;
+  if (F == 0) return ESI_OK;
+  if (!tf || !out) return ESI_ERR_INVALID_ARG;
+  for (size_t j = 1; j < F; ++j)
+    if (tf[j] < tf[j - 1]) return ESI_ERR_INVALID_ARG;
+  if (tf[0] < h->prm.t_origin_us || (h->has_last_frame && tf[0] < h->last_frame_t))
+    return ESI_ERR_NEGATIVE_INTERVAL;
+  if (F > (size_t)INT32_MAX) return ESI_ERR_INVALID_ARG;
+  cudaSetDevice(h->prm.device);
+  cudaStream_t st = h->stream;
+  const int64_t t_cap = tf[F - 1];
+  h->st_launches = 0;
+  h->st_events = 0;
+  h->st_chunks = 0;
+
+  // frame times -> device
+  int rc = ensure_dev(h, &h->d_tf, &h->tf_cap, F);
+  if (rc) return rc;
+  ESI_CUDA(h, cudaMemcpyAsync(h->d_tf, tf, F * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+
+  // output: device pointer written in place, host pointer staged
+  const bool out_dev = is_device_ptr(out);
+  const size_t frame_bytes = (size_t)F * (size_t)h->P;
+  uint8_t* dout = out;
+  if (!out_dev) {
+    if (frame_bytes > h->frames_cap) {
+      if (h->d_frames) cudaFree(h->d_frames);
+      h->d_frames = nullptr;
+      h->frames_cap = 0;
+      if (cudaMalloc((void**)&h->d_frames, frame_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return ESI_ERR_OOM;
+      }
+      h->frames_cap = frame_bytes;
+    }
+    dout = h->d_frames;
+  }
+  const int vec8 = (h->P % 8 == 0) && (((uintptr_t)dout & 7) == 0);
+
+  // chunk plan over the pending segments
+  std::vector<Chunk> chunks;
+  for (int k = 0; k < (int)h->segs.size(); ++k)
+    for (int64_t off = 0; off < h->segs[k].n; off += h->chunk_events)
+      chunks.push_back({h->segs[k].ptr + off, std::min(h->chunk_events, h->segs[k].n - off), k});
+
+  if (chunks.empty()) {
+    ReadoutArgs ra{h->dS, h->dT, h->d_tf, (int32_t)F, dout, h->P, vec8, h->dp, h->mp};
+    TimedLaunch tl;
+    timed_begin(h, 2, &tl);
+    ESI_CUDA(h, launch_readout(ra, st));
+    timed_end(h, &tl);
+    h->st_launches = 1;
+  } else {
+    rc = ensure_dev(h, &h->d_chunk_first, &h->cf_cap, chunks.size());
+    if (rc) return rc;
+    rc = ensure_pinned(h, chunks.size() * sizeof(void*) + h->segs.size() * sizeof(int64_t) + 128);
+    if (rc) return rc;
+    const esi_event_t** hcf = (const esi_event_t**)h->h_pin;
+    for (size_t c = 0; c < chunks.size(); ++c) hcf[c] = chunks[c].ptr;
+    ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_first, hcf, chunks.size() * sizeof(void*), cudaMemcpyHostToDevice, st));
+    ESI_CUDA(h, launch_plan(h->d_chunk_first, (int)chunks.size(), t_cap, h->d_n_active, st));
+    int32_t* hna = (int32_t*)(h->h_pin + chunks.size() * sizeof(void*) + 16);
+    ESI_CUDA(h, cudaMemcpyAsync(hna, h->d_n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    ESI_CUDA(h, cudaStreamSynchronize(st));
+    const int n_act = std::max(1, *hna);
+    ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
+
+    int64_t index_base = 0;
+    for (int c = 0; c < n_act; ++c) {
+      const Chunk& ch = chunks[c];
+      const int n_tiles = (int)((ch.n + kTile - 1) / kTile);
+      PartArgs pa;
+      pa.ev = ch.ptr;
+      pa.n = ch.n;
+      pa.index_base = index_base;
+      pa.prev_t = (c == 0) ? h->d_last_t : &chunks[c - 1].ptr[chunks[c - 1].n - 1].t_us;
+      pa.t_origin = h->prm.t_origin_us;
+      pa.last_frame_t = h->has_last_frame ? h->last_frame_t : INT64_MIN;
+      pa.t_cap = t_cap;
+      pa.W = h->W;
+      pa.H = h->H;
+      pa.band_shift = h->band_shift;
+      pa.nb = h->nb;
+      pa.nb_bits = h->nb_bits;
+      pa.rec = h->rec;
+      pa.meta = h->meta;
+      pa.tile_t0 = h->tile_t0;
+      pa.tile_wide = h->tile_wide;
+      pa.wide_t = h->wide_t;
+      pa.err = h->d_err;
+      TimedLaunch t1;
+      timed_begin(h, 0, &t1);
+      ESI_CUDA(h, launch_partition(pa, n_tiles, st));
+      timed_end(h, &t1);
+
+      IntArgs ia;
+      ia.rec = h->rec;
+      ia.meta = h->meta;
+      ia.tile_t0 = h->tile_t0;
+      ia.tile_wide = h->tile_wide;
+      ia.wide_t = h->wide_t;
+      ia.n_tiles = n_tiles;
+      ia.first_chunk = (c == 0);
+      ia.n = ch.n;
+      ia.ev = ch.ptr;
+      ia.ev_next = (c + 1 < (int)chunks.size()) ? chunks[c + 1].ptr : nullptr;
+      ia.tf = h->d_tf;
+      ia.F = (int32_t)F;
+      ia.t_cap = t_cap;
+      ia.S = h->dS;
+      ia.T = h->dT;
+      ia.out = dout;
+      ia.P = h->P;
+      ia.band_px = h->band_px;
+      ia.nb = h->nb;
+      ia.vec8 = vec8;
+      ia.dp = h->dp;
+      ia.mp = h->mp;
+      TimedLaunch t2;
+      timed_begin(h, 1, &t2);
+      ESI_CUDA(h, launch_integrate(ia, st));
+      timed_end(h, &t2);
+      h->st_launches += 2;
+      h->st_chunks += 1;
+      index_base += ch.n;
+    }
+    // consumed events per segment (segments after the last active chunk consume none)
+    const int last_seg = chunks[n_act - 1].seg;
+    rc = ensure_dev(h, &h->d_cons, &h->cons_cap, h->segs.size());
+    if (rc) return rc;
+    for (int k = 0; k <= last_seg; ++k) {
+      ESI_CUDA(h, launch_consume(h->segs[k].ptr, h->segs[k].n, t_cap, h->d_cons + k, h->d_last_t, st));
+      h->st_launches += 1;
+    }
+    int64_t* hcons = (int64_t*)h->h_pin;
+    unsigned long long* herr = (unsigned long long*)(h->h_pin + (last_seg + 1) * sizeof(int64_t));
+    ESI_CUDA(h, cudaMemcpyAsync(hcons, h->d_cons, (last_seg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    ESI_CUDA(h, cudaMemcpyAsync(herr, h->d_err, sizeof(*herr), cudaMemcpyDeviceToHost, st));
+    ESI_CUDA(h, cudaStreamSynchronize(st));
+    if (*herr != kNoError) h->sticky = (int)(*herr & 0xff);
+    std::vector<Segment> keep;
+    for (int k = 0; k < (int)h->segs.size(); ++k) {
+      Segment s = h->segs[k];
+      const int64_t cons = k <= last_seg ? hcons[k] : 0;
+      h->st_events += cons;
+      if (cons >= s.n) {
+        pool_give(h, s.owned, s.owned_bytes);
+        continue;
+      }
+      s.ptr += cons;
+      s.n -= cons;
+      keep.push_back(s);
+    }
+    h->segs.swap(keep);
+  }
+  if (!out_dev) ESI_CUDA(h, cudaMemcpyAsync(out, dout, frame_bytes, cudaMemcpyDeviceToHost, st));
+  ESI_CUDA(h, cudaStreamSynchronize(st));
+  collect_timing(h);
+  h->has_last_frame = true;
+  h->last_frame_t = t_cap;
+  return h->sticky;
+}
+
+int esi_render(esi_handle_t* h, int64_t t_frame_us, uint8_t* out) {
+  return esi_render_many(h, &t_frame_us, 1, out);
+}
+
+int esi_get_state(esi_handle_t* h, float* S, int64_t* T) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  cudaSetDevice(h->prm.device);
+  if (S) ESI_CUDA(h, cudaMemcpyAsync(S, h->dS, h->P * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  if (T) ESI_CUDA(h, cudaMemcpyAsync(T, h->dT, h->P * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaStreamSynchronize(h->stream));
+  return h->sticky;
+}
+
+int esi_set_state(esi_handle_t* h, const float* S, const int64_t* T) {
+  if (!h || !S || !T) return ESI_ERR_INVALID_ARG;
+  if (h->sticky) return h->sticky;
+  cudaSetDevice(h->prm.device);
+  ESI_CUDA(h, cudaMemcpyAsync(h->dS, S, h->P * sizeof(float), cudaMemcpyHostToDevice, h->stream));
+  ESI_CUDA(h, cudaMemcpyAsync(h->dT, T, h->P * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+  ESI_CUDA(h, cudaStreamSynchronize(h->stream));
+  return ESI_OK;
+}
+
+int esi_enable_kernel_timing(esi_handle_t* h, int enable) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  h->timing = enable != 0;
+  for (int i = 0; i < 4; ++i) { h->kt_ms[i] = 0; h->kt_n[i] = 0; }
+  return ESI_OK;
+}
+
+int esi_kernel_time(esi_handle_t* h, int kind, double* ms_total, int64_t* launches) {
+  if (!h || kind < 0 || kind > 3) return ESI_ERR_INVALID_ARG;
+  if (ms_total) *ms_total = h->kt_ms[kind];
+  if (launches) *launches = h->kt_n[kind];
+  return ESI_OK;
+}
+
+int esi_last_render_stats(esi_handle_t* h, int64_t* launches, int64_t* events, int64_t* chunks) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  if (launches) *launches = h->st_launches;
+  if (events) *events = h->st_events;
+  if (chunks) *chunks = h->st_chunks;
+  return ESI_OK;
+}
+
+int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8_t* out_p,
+                        size_t n_out, uint32_t* band_start, int32_t* nb_out, int32_t* band_px_out) {
+  if (!h || !band_start || !nb_out || !band_px_out) return ESI_ERR_INVALID_ARG;
+  if (h->sticky) return h->sticky;
+  cudaSetDevice(h->prm.device);
+  *nb_out = h->nb;
+  *band_px_out = h->band_px;
+  if (h->segs.empty()) {
+    for (int b = 0; b <= h->nb; ++b) band_start[b] = 0;
+    return ESI_OK;
+  }
+  const Segment& s = h->segs[0];
+  const int64_t n = std::min(h->chunk_events, s.n);
+  if ((int64_t)n_out < n || !out_t || !out_pid || !out_p) return ESI_ERR_INVALID_ARG;
+  const int n_tiles = (int)((n + kTile - 1) / kTile);
+  PartArgs pa;
+  pa.ev = s.ptr;
+  pa.n = n;
+  pa.index_base = 0;
+  pa.prev_t = h->d_last_t;
+  pa.t_origin = h->prm.t_origin_us;
+  pa.last_frame_t = h->has_last_frame ? h->last_frame_t : INT64_MIN;
+  pa.t_cap = INT64_MAX;
+  pa.W = h->W;
+  pa.H = h->H;
+  pa.band_shift = h->band_shift;
+  pa.nb = h->nb;
+  pa.nb_bits = h->nb_bits;
+  pa.rec = h->rec;
+  pa.meta = h->meta;
+  pa.tile_t0 = h->tile_t0;
+  pa.tile_wide = h->tile_wide;
+  pa.wide_t = h->wide_t;
+  pa.err = h->d_err;
+  ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), h->stream));
+  ESI_CUDA(h, launch_partition(pa, n_tiles, h->stream));
+  std::vector<uint2> rec(n_tiles * (size_t)kTile);
+  std::vector<uint32_t> meta((size_t)h->nb * n_tiles);
+  std::vector<int64_t> t0(n_tiles), wt;
+  std::vector<int32_t> wide(n_tiles);
+  ESI_CUDA(h, cudaMemcpyAsync(rec.data(), h->rec, n * sizeof(uint2), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaMemcpyAsync(meta.data(), h->meta, meta.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaMemcpyAsync(t0.data(), h->tile_t0, n_tiles * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaMemcpyAsync(wide.data(), h->tile_wide, n_tiles * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaStreamSynchronize(h->stream));
+  bool any_wide = false;
+  for (int t = 0; t < n_tiles; ++t) any_wide |= wide[t] != 0;
+  if (any_wide) {
+    wt.resize(n);
+    ESI_CUDA(h, cudaMemcpy(wt.data(), h->wide_t, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  }
+  size_t o = 0;
+  for (int b = 0; b < h->nb; ++b) {
+    band_start[b] = (uint32_t)o;
+    for (int t = 0; t < n_tiles; ++t) {
+      const uint32_t m = meta[(size_t)b * n_tiles + t];
+      const uint32_t off = m & 0xffffu, cnt = m >> 16;
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const size_t idx = (size_t)t * kTile + off + i;
+        const uint2 r = rec[idx];
+        const int64_t tt = wide[t] ? wt[idx] : t0[t] + (int64_t)(uint32_t)(r.x - (uint32_t)t0[t]);
+        out_t[o] = tt;
+        out_pid[o] = (uint32_t)b * h->band_px + (r.y & 0x7fffffffu);
+        out_p[o] = (r.y & 0x80000000u) ? -1 : 1;
+        ++o;
+      }
+    }
+  }
+  band_start[h->nb] = (uint32_t)o;
+  return ESI_OK;
+}
+
+}  // extern "C"

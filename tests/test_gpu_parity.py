@@ -1,0 +1,324 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Bars (BASELINE.json north_star): grouping bit-exact;
+T exact; S within 1e-6 abs or 1e-5 rel; frames within +-1 LSB on <= 0.01 %
+of pixel-frames."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from esi_synth import make_workload, to_numpy_struct, from_numpy_struct, events_of_pixels
+from helpers import (assert_frames_close, assert_state_close, gpu_run, oracle_run, ev_np_of)
+
+pytestmark = pytest.mark.gpu
+
+_CACHE = {}
+
+
+def wl(name, **kw):
+    key = (name, tuple(sorted(kw.items())))
+    if key not in _CACHE:
+        _CACHE[key] = make_workload(name, "cpu", **kw)
+    return _CACHE[key]
+
+
+def mk_events(rows):
+    a = np.zeros(len(rows), dtype=[("t", "<i8"), ("x", "<u2"), ("y", "<u2"), ("p", "i1"), ("_pad", "u1", (3,))])
+    for i, r in enumerate(rows):
+        a[i]["t"], a[i]["x"], a[i]["y"], a[i]["p"] = r
+    return a
+
+
+def random_stream(seed, W, H, n, span, hot=0.0, cluster=True):
+    rng = np.random.default_rng(seed)
+    t = np.sort(rng.integers(0, span, n)).astype(np.int64)
+    if cluster:
+        x = (rng.integers(0, W, n) // 3 * 3 % W).astype(np.uint16)
+    else:
+        x = rng.integers(0, W, n).astype(np.uint16)
+    y = rng.integers(0, H, n).astype(np.uint16)
+    if hot > 0:
+        m = rng.random(n) < hot
+        x[m] = W // 2
+        y[m] = H // 2
+    p = rng.choice([-1, 1], n).astype(np.int8)
+    a = np.zeros(n, dtype=[("t", "<i8"), ("x", "<u2"), ("y", "<u2"), ("p", "i1"), ("_pad", "u1", (3,))])
+    a["t"], a["x"], a["y"], a["p"] = t, x, y, p
+    return a
+
+
+def check(W, H, ev_np, tf, params, **kw):
+    f_ref, S_ref, T_ref = oracle_run(W, H, ev_np, tf, params, readout_decay=kw.get("readout_decay", 1),
+                                     t_origin=kw.get("t_origin", 0))
+    f_gpu, S_gpu, T_gpu, stats = gpu_run(W, H, from_numpy_struct(ev_np), tf, params, **kw)
+    assert_state_close(S_gpu, T_gpu, S_ref, T_ref)
+    frac = assert_frames_close(f_gpu, f_ref)
+    return frac, stats
+
+
+DEF = {"C": 0.15, "k": 10.0, "b": 2.0, "s_min": -1.5, "s_max": 1.5}
+
+
+def test_c1_full():
+    w = wl("c1")
+    check(w.W, w.H, ev_np_of(w), w.t_frames, w.params)
+
+
+def test_c1_many_chunks():
+    w = wl("c1")
+    frac, stats = check(w.W, w.H, ev_np_of(w), w.t_frames, w.params, chunk_events=8192)
+    assert stats["chunks"] >= 10
+
+
+def test_c2_full():
+    w = wl("c2")
+    check(w.W, w.H, ev_np_of(w), w.t_frames, w.params)
+
+
+def test_c3_hot_pixels():
+    w = wl("c3", duration_us=1_000_000)
+    check(w.W, w.H, ev_np_of(w), w.t_frames, w.params)
+
+
+@pytest.mark.parametrize("b", [2.0, 1.0, 2.5, 0.5, 3.0])
+@pytest.mark.parametrize("k", [10.0, 100.0])
+@pytest.mark.parametrize("rd", [1, 0])
+def test_parameter_matrix(b, k, rd):
+    ev = random_stream(int(b * 10 + k + rd), 40, 30, 60_000, 600_000)
+    prm = dict(DEF, b=b, k=k)
+    tf = np.arange(1, 61, dtype=np.int64) * 10_000
+    check(40, 30, ev, tf, prm, readout_decay=rd)
+
+
+@pytest.mark.parametrize("lo,hi", [(-0.3, 0.3), (-0.2, 1.0), (0.1, 2.0), (-2.0, -0.05)])
+def test_tight_and_asymmetric_clamps(lo, hi):
+    ev = random_stream(7, 33, 17, 50_000, 300_000, hot=0.05)
+    prm = dict(DEF, s_min=lo, s_max=hi)
+    check(33, 17, ev, np.arange(1, 31, dtype=np.int64) * 10_000, prm, chunk_events=16384)
+
+
+def test_dense_hot_pixel_and_ties():
+    # one pixel receives 40 % of all events, many equal timestamps
+    rng = np.random.default_rng(3)
+    ev = random_stream(3, 64, 64, 200_000, 200_000, hot=0.4)
+    ev["t"] = np.sort(ev["t"] // 7 * 7)
+    check(64, 64, ev, np.arange(1, 201, dtype=np.int64) * 1000, DEF, chunk_events=65536)
+
+
+def test_frame_ties_and_empty_windows():
+    ev = mk_events([(10_000, 1, 1, 1), (10_000, 1, 1, 1), (10_000, 2, 0, -1), (20_000, 1, 1, 1),
+                    (55_000, 1, 1, -1), (55_001, 1, 1, 1)])
+    tf = np.array([5_000, 10_000, 10_000, 20_000, 30_000, 40_000, 55_000, 55_000, 200_000], np.int64)
+    check(4, 3, ev, tf, DEF)
+
+
+def test_odd_sizes_and_unaligned_frames():
+    for (W, H) in [(65, 3), (1, 1), (7, 300), (257, 5), (1000, 3)]:
+        ev = random_stream(W * H, W, H, 20_000, 200_000)
+        check(W, H, ev, np.arange(1, 21, dtype=np.int64) * 10_000, DEF)
+
+
+def test_no_events_baseline_and_readout_only():
+    ev = mk_events([])
+    f_gpu, S, T, _ = gpu_run(9, 5, from_numpy_struct(ev), np.array([1, 2, 3], np.int64), DEF)
+    assert (f_gpu == 128).all() and (S == 0).all() and (T == 0).all()
+
+
+def test_events_after_last_frame_stay_pending():
+    from paper_2508_02238_b200 import Esi
+    ev = random_stream(11, 20, 10, 30_000, 300_000)
+    tf = np.arange(1, 31, dtype=np.int64) * 10_000
+    f_ref, S_ref, T_ref = oracle_run(20, 10, ev, tf, DEF)
+    e = Esi(20, 10)
+    try:
+        d = from_numpy_struct(ev).cuda()
+        assert e.push(d) == 0
+        out = []
+        for j in range(0, 30, 7):                # several render calls, events pending in between
+            out.append(e.render_many(tf[j:j + 7]))
+        f = np.concatenate(out)
+        S, T = e.get_state()
+    finally:
+        e.close()
+    assert_frames_close(f, f_ref)
+    assert_state_close(S, T, S_ref, T_ref)
+
+
+def test_render_many_equals_repeated_render_bit_exact():
+    from paper_2508_02238_b200 import Esi
+    ev = random_stream(12, 50, 40, 40_000, 400_000)
+    tf = np.arange(1, 41, dtype=np.int64) * 10_000
+    d = from_numpy_struct(ev).cuda()
+    a = Esi(50, 40)
+    b = Esi(50, 40)
+    try:
+        a.push(d)
+        fa = a.render_many(tf)
+        b.push(d)
+        fb = np.stack([b.render(int(t)) for t in tf])
+        Sa, Ta = a.get_state()
+        Sb, Tb = b.get_state()
+    finally:
+        a.close(); b.close()
+    assert np.array_equal(fa, fb)
+    assert np.array_equal(Sa, Sb) and np.array_equal(Ta, Tb)
+
+
+def test_interleaved_push_render_and_host_paths():
+    from paper_2508_02238_b200 import Esi
+    ev = random_stream(13, 30, 20, 50_000, 500_000)
+    tf = np.arange(1, 51, dtype=np.int64) * 10_000
+    f_ref, S_ref, T_ref = oracle_run(30, 20, ev, tf, DEF)
+    e = Esi(30, 20)
+    try:
+        out = []
+        for j in range(50):
+            lo = tf[j - 1] if j else -1
+            m = (ev["t"] > lo) & (ev["t"] <= tf[j])
+            assert e.push(np.ascontiguousarray(ev[m])) == 0          # host push (copied)
+            out.append(e.render(int(tf[j])))                          # host output
+        S, T = e.get_state()
+    finally:
+        e.close()
+    assert_frames_close(np.stack(out), f_ref)
+    assert_state_close(S, T, S_ref, T_ref)
+
+
+def test_wide_time_gaps():
+    # gaps > 2^32 us inside one chunk / tile exercise the wide-tile path
+    big = 1 << 33
+    rows = []
+    for i in range(3000):
+        rows.append((i * 37 + (big if i >= 1500 else 0) + (2 * big if i >= 2500 else 0), i % 7, i % 5, 1 if i % 3 else -1))
+    ev = mk_events(rows)
+    tf = np.array([1000, 60_000, big + 30_000, big + 60_000, 3 * big + 10, 3 * big + 200_000], np.int64)
+    check(7, 5, ev, tf, DEF)
+
+
+def test_t_origin_and_late_start():
+    ev = random_stream(14, 16, 16, 20_000, 300_000)
+    ev["t"] += 5_000_000_000
+    tf = 5_000_000_000 + np.arange(1, 31, dtype=np.int64) * 10_000
+    check(16, 16, ev, tf, DEF, t_origin=5_000_000_000 - 40_000)
+
+
+def test_partition_is_bit_exact_stable_grouping():
+    from paper_2508_02238_b200 import Esi
+    for (W, H, n) in [(64, 48, 100_000), (346, 260, 300_000), (1280, 720, 2_000_000)]:
+        ev = random_stream(W, W, H, n, 1_000_000, cluster=False)
+        e = Esi(W, H)
+        try:
+            e.push(from_numpy_struct(ev).cuda())
+            t, pid, p, bs, band_px = e.debug_partition(n)
+        finally:
+            e.close()
+        m = min(n, 4 << 20)
+        ref_pid = ev["y"][:m].astype(np.int64) * W + ev["x"][:m]
+        perm = oracle.stable_group_by(ref_pid // band_px)     # stable sort by band
+        np.testing.assert_array_equal(t, ev["t"][:m][perm])
+        np.testing.assert_array_equal(pid, ref_pid[perm])
+        np.testing.assert_array_equal(p, ev["p"][:m][perm])
+        # per-band CSR offsets
+        counts = np.bincount(ref_pid // band_px, minlength=len(bs) - 1)
+        np.testing.assert_array_equal(np.diff(bs), counts)
+
+
+def test_errors_are_reported():
+    from paper_2508_02238_b200 import Esi, esi
+    W, H = 8, 6
+    for rows, code in [([(5, 8, 0, 1)], esi.ESI_ERR_OUT_OF_BOUNDS),
+                       ([(5, 0, 6, 1)], esi.ESI_ERR_OUT_OF_BOUNDS),
+                       ([(5, 1, 1, 0)], esi.ESI_ERR_BAD_POLARITY),
+                       ([(5, 1, 1, 1), (4, 1, 1, 1)], esi.ESI_ERR_NEGATIVE_INTERVAL)]:
+        e = Esi(W, H)
+        try:
+            assert e.push(from_numpy_struct(mk_events(rows)).cuda()) == 0   # lazy validation
+            out = torch.empty((1, H, W), dtype=torch.uint8, device="cuda")
+            assert e.render_many_rc([100], out) == code
+            assert e.error() == code                                       # sticky
+            e.reset()
+            assert e.error() == 0
+        finally:
+            e.close()
+        e = Esi(W, H, validate_on_push=1)                                  # eager, atomic
+        try:
+            assert e.push(from_numpy_struct(mk_events(rows)).cuda()) == code
+            assert e.error() == 0
+            f = e.render_many([100])
+            assert (f == 128).all()
+        finally:
+            e.close()
+    # first error in stream order wins, as in the oracle
+    e = Esi(W, H)
+    try:
+        e.push(from_numpy_struct(mk_events([(1, 1, 1, 1), (2, 1, 1, 5), (3, 9, 9, 1)])).cuda())
+        assert e.render_many_rc([10], np.empty((1, H, W), np.uint8)) == esi.ESI_ERR_BAD_POLARITY
+    finally:
+        e.close()
+    # events not later than the last rendered frame, frames going back in time
+    e = Esi(W, H)
+    try:
+        e.push(from_numpy_struct(mk_events([(1, 1, 1, 1)])).cuda())
+        e.render_many([10])
+        assert e.render_many_rc([5], np.empty((1, H, W), np.uint8)) == esi.ESI_ERR_NEGATIVE_INTERVAL
+        e.push(from_numpy_struct(mk_events([(10, 1, 1, 1)])).cuda())
+        assert e.render_many_rc([20], np.empty((1, H, W), np.uint8)) == esi.ESI_ERR_NEGATIVE_INTERVAL
+    finally:
+        e.close()
+
+
+def test_checkpoint_resume_equals_whole_stream():
+    from paper_2508_02238_b200 import Esi
+    ev = random_stream(15, 24, 24, 40_000, 400_000)
+    tf = np.arange(1, 41, dtype=np.int64) * 10_000
+    f_all, S_all, T_all, _ = gpu_run(24, 24, from_numpy_struct(ev), tf, DEF)
+    cut = 17
+    a = Esi(24, 24)
+    b = Esi(24, 24)
+    try:
+        m = ev["t"] <= tf[cut - 1]
+        a.push(from_numpy_struct(ev[m]).cuda())
+        f1 = a.render_many(tf[:cut])
+        S, T = a.get_state()
+        b.set_state(S, T)
+        b.push(from_numpy_struct(ev[~m]).cuda())
+        # b has never rendered: frames continue from the checkpoint
+        f2 = b.render_many(tf[cut:])
+        S2, T2 = b.get_state()
+    finally:
+        a.close(); b.close()
+    assert np.array_equal(np.concatenate([f1, f2]), f_all)
+    assert np.array_equal(S2, S_all) and np.array_equal(T2, T_all)
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled():
+    """c4 at full size (200 M events, 1000 frames) in the bench's launch
+    configuration; 3000 sampled pixels checked against the oracle one by one."""
+    w = make_workload("c4", "cuda")
+    W, H = w.W, w.H
+    from paper_2508_02238_b200 import Esi
+    e = Esi(W, H, **w.params)
+    try:
+        out = torch.empty((len(w.t_frames), H, W), dtype=torch.uint8, device="cuda")
+        assert e.push(w.events) == 0
+        e.render_many(w.t_frames, out)
+        S, T = e.get_state()
+    finally:
+        e.close()
+    ev_np = to_numpy_struct(w.events)
+    rng = np.random.default_rng(4)
+    pix = np.unique(rng.integers(0, W * H, 3000))
+    sub = events_of_pixels(ev_np, W, pix)
+    # remap the sampled pixels onto a 1-row sensor for the oracle
+    pid = sub["y"].astype(np.int64) * W + sub["x"]
+    col = np.searchsorted(pix, pid)
+    sub2 = sub.copy()
+    sub2["x"] = col.astype(np.uint16)
+    sub2["y"] = 0
+    f_ref, S_ref, T_ref = oracle_run(len(pix), 1, sub2, w.t_frames, w.params)
+    f_gpu = out.reshape(len(w.t_frames), -1)[:, torch.as_tensor(pix, device="cuda")].cpu().numpy()
+    assert_frames_close(f_gpu, f_ref[:, 0, :])
+    assert_state_close(S.reshape(-1)[pix], T.reshape(-1)[pix], S_ref[0], T_ref[0])
+    # every pixel: frame values in range, state within the clamp bounds
+    assert float(np.abs(S).max()) <= w.params["s_max"] + 1e-6
