@@ -364,6 +364,13 @@ def _rotation(W, H, device, seed, duration_us, rate_fn, c=0.15, dt_us=500, name=
     L0 = sc.L(torch.tensor([0.0], device=device))
     L1 = sc.L(torch.tensor([d], device=device))
     ev_per_rad = float((L1 - L0).abs().sum()) / d / c
+    # the reference-level model loses crossings to hysteresis: calibrate the count
+    # per radian with a short count-only run, then scale omega
+    # (steady state only: the first 0.1 rad charges the reference levels up)
+    def count(rad):
+        return simulate(sc.L, lambda ts: ts.astype(np.float64) * 1e-6, 0, int(rad * 1e6), 1000, c, device,
+                        count_only=True)
+    ev_per_rad = max(1.0, (count(0.4) - count(0.1)) / 0.3)
     # theta(t) = integral of omega, omega(t) = rate(t) / ev_per_rad
     tt = np.arange(0, duration_us + dt_us, dt_us, dtype=np.int64)
     rates = rate_fn(tt)

@@ -46,20 +46,43 @@ cudaError_t launch_readout(const ReadoutArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-__global__ void esi_plan_kernel(const esi_event_t* const* chunk_first, int n_chunks, int64_t t_cap,
-                                int32_t* n_active) {
-  // chunk first-event times are non-decreasing: count those <= t_cap
-  int lo = 0, hi = n_chunks;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (chunk_first[mid]->t_us <= t_cap) lo = mid + 1; else hi = mid;
+__global__ void esi_plan_kernel(const esi_event_t* const* chunk_first, const int64_t* chunk_n,
+                                int n_chunks, const int64_t* tf, int F, int64_t t_cap, int allow_fast,
+                                ChunkInfo* info, int32_t* n_active) {
+  // chunk c renders the frames j with t_first(c) <= t_j < t_first(c+1) (chunk 0: t_j < t_first(1))
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_chunks; c += gridDim.x * blockDim.x) {
+    const esi_event_t* ev = chunk_first[c];
+    const int64_t t0 = ev[0].t_us;
+    const int64_t t1 = ev[chunk_n[c] - 1].t_us;
+    ChunkInfo ci;
+    ci.tbase = t0;
+    ci.f_lo = c == 0 ? 0 : lower_bound_i64(tf, F, t0);
+    ci.f_hi = c + 1 < n_chunks ? lower_bound_i64(tf, F, chunk_first[c + 1]->t_us) : F;
+    ci.active = t0 <= t_cap;
+    ci.wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
+    int64_t lo = t0, hi = t1;
+    if (ci.f_lo < ci.f_hi) {
+      lo = min(lo, tf[ci.f_lo]);
+      hi = max(hi, tf[ci.f_hi - 1]);
+    }
+    ci.trel = lo;
+    ci.fast = allow_fast && (hi - lo) < ((int64_t)1 << 30);
+    ci._pad = 0;
+    info[c] = ci;
+    // first events are non-decreasing: the active chunks are a prefix
+    const bool next_active = c + 1 < n_chunks && chunk_first[c + 1]->t_us <= t_cap;
+    if (ci.active && !next_active) *n_active = c + 1;
+    if (c == 0 && !ci.active) *n_active = 0;
   }
-  *n_active = lo;
 }
 
-cudaError_t launch_plan(const esi_event_t* const* chunk_first, int n_chunks, int64_t t_cap,
+cudaError_t launch_plan(const esi_event_t* const* chunk_first, const int64_t* chunk_n, int n_chunks,
+                        const int64_t* tf, int F, int64_t t_cap, int allow_fast, ChunkInfo* info,
                         int32_t* n_active, cudaStream_t s) {
-  esi_plan_kernel<<<1, 1, 0, s>>>(chunk_first, n_chunks, t_cap, n_active);
+  const int threads = 128;
+  const int blocks = (n_chunks + threads - 1) / threads;
+  esi_plan_kernel<<<blocks, threads, 0, s>>>(chunk_first, chunk_n, n_chunks, tf, F, t_cap, allow_fast, info,
+                                             n_active);
   return cudaGetLastError();
 }
 

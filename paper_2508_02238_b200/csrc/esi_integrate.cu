@@ -1,5 +1,7 @@
-// esi_integrate.cu -- K2: per-band integration (Alg. 2) fused with the frame
-// readout (Eq. 14) for every frame of the chunk.
+// esi_integrate.cu -- K2 (general variant): per-band integration (Alg. 2) fused
+// with the frame readout (Eq. 14) for every frame of the chunk, with 64-bit
+// times throughout.  Used for chunks the fast kernel (esi_integrate_fast.cu)
+// cannot take: spans >= 2^30 us, decay horizons >= 2^23 us (k < 0.12 /s).
 //
 // One CTA per band of BP = NW*256 consecutive pixel ids; warp w owns the
 // 256-pixel sub-band [w*256, w*256+256) and lane l its 8 pixels.  The band's
@@ -27,9 +29,9 @@ namespace esi {
 
 size_t integrate_smem_bytes(int band_px) {
   const int nw = band_px / kWarpPx;
-  return (size_t)band_px * (sizeof(int64_t) + sizeof(float) + sizeof(int32_t)) +
+  return (size_t)band_px * (sizeof(int64_t) + sizeof(double) + sizeof(int32_t)) +
          (size_t)kSubBatch * (sizeof(int64_t) + sizeof(uint32_t)) +
-         (size_t)(kMaxTilesPerChunk + 1) * sizeof(uint32_t) +
+         (size_t)(2 * kMaxTilesPerChunk + 1) * sizeof(uint32_t) +
          (size_t)nw * kSubBatch * sizeof(uint16_t) + 64;
 }
 
@@ -37,13 +39,29 @@ template <int NW>
 struct IntCtx {
   static constexpr int BP = NW * kWarpPx;
   int64_t* Tsm;
-  float* Ssm;
+  double* Ssm;
   int32_t* tag;
   int64_t* At;
   uint32_t* Apr;
-  uint32_t* pre;
+  uint32_t* pre;   // [n_tiles + 1] exclusive prefix of the band's per-tile counts
+  uint32_t* mt;    // [n_tiles] meta (offset | count << 16)
   uint16_t* L;
 };
+
+// Eq. 4 in fp64 (reading A14: d = 0 exactly from dt_cut = ceil(1e6/k) on)
+__device__ __forceinline__ double wide_decay(int64_t dt, const WideParams& wp) {
+  if (dt >= wp.dt_cut) return 0.0;
+  const double u = 1.0 - wp.k_us * (double)dt;
+  if (u <= 0.0) return 0.0;
+  return wp.bmode == 2 ? u * u : pow(u, wp.b);
+}
+
+// Eq. 13 + Eq. 14 in fp64, rounded half away from zero (reading A8).
+__device__ __forceinline__ uint32_t wide_map8(double v, const WideParams& wp) {
+  v = fmin(fmax(v, wp.smin), wp.smax);
+  const int q = (int)floor(v * wp.scale + wp.off5);
+  return (uint32_t)min(max(q, 0), 255);
+}
 
 template <int NW>
 __device__ __forceinline__ void warp_readout(const IntArgs& a, const IntCtx<NW>& c, int j,
@@ -51,15 +69,12 @@ __device__ __forceinline__ void warp_readout(const IntArgs& a, const IntCtx<NW>&
   const int base = warp * kWarpPx + lane * 8;
   if (base >= npx) return;
   const int64_t tj = a.tf[j];
-  const float4 s0 = *reinterpret_cast<const float4*>(c.Ssm + base);
-  const float4 s1 = *reinterpret_cast<const float4*>(c.Ssm + base + 4);
-  const float s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
   uint32_t bytes[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    float v = s[q];
-    if (a.mp.readout_decay) v *= esi_decay(tj - c.Tsm[base + q], a.dp);
-    bytes[q] = esi_map8(v, a.mp);
+    double v = c.Ssm[base + q];
+    if (a.wp.readout_decay) v *= wide_decay(tj - c.Tsm[base + q], a.wp);
+    bytes[q] = wide_map8(v, a.wp);
   }
   uint8_t* dst = a.out + (int64_t)j * a.P + px0 + base;
   if (a.vec8 && base + 8 <= npx) {
@@ -72,41 +87,21 @@ __device__ __forceinline__ void warp_readout(const IntArgs& a, const IntCtx<NW>&
   }
 }
 
-// t of the band event at band position q (thread-local helper, cold path)
-__device__ int64_t band_event_time(const IntArgs& a, const uint32_t* pre, int band, int q,
-                                   int wide_chunk, int64_t tbase) {
-  int lo = 0, hi = a.n_tiles;  // largest t with pre[t] <= q
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (pre[mid] <= (uint32_t)q) lo = mid; else hi = mid;
-  }
-  // skip empty tiles (pre[lo] == pre[lo+1])
-  while (pre[lo + 1] <= (uint32_t)q) ++lo;
-  const uint32_t m = a.meta[(int64_t)band * a.n_tiles + lo];
-  const int64_t idx = (int64_t)lo * kTile + (m & 0xffffu) + (q - pre[lo]);
-  if (wide_chunk) {
-    if (a.tile_wide[lo]) return a.wide_t[idx];
-    const int64_t t0 = a.tile_t0[lo];
-    return t0 + (int64_t)(uint32_t)(a.rec[idx].x - (uint32_t)t0);
-  }
-  return tbase + (int64_t)(uint32_t)(a.rec[idx].x - (uint32_t)tbase);
-}
-
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) esi_integrate_kernel(IntArgs a) {
+__global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) {
   constexpr int BP = NW * kWarpPx;
   constexpr int NT = NW * 32;
   extern __shared__ __align__(16) unsigned char smem[];
   IntCtx<NW> c;
   c.Tsm = reinterpret_cast<int64_t*>(smem);
   c.At = c.Tsm + BP;
-  c.Ssm = reinterpret_cast<float*>(c.At + kSubBatch);
+  c.Ssm = reinterpret_cast<double*>(c.At + kSubBatch);
   c.tag = reinterpret_cast<int32_t*>(c.Ssm + BP);
   c.Apr = reinterpret_cast<uint32_t*>(c.tag + BP);
   c.pre = c.Apr + kSubBatch;
-  c.L = reinterpret_cast<uint16_t*>(c.pre + kMaxTilesPerChunk + 1);
-  __shared__ int s_flo, s_fhi, s_active, s_wide;
-  __shared__ int64_t s_tbase, s_tnext;
+  c.mt = c.pre + kMaxTilesPerChunk + 1;
+  c.L = reinterpret_cast<uint16_t*>(c.mt + kMaxTilesPerChunk);
+  __shared__ int64_t s_tnext;
   __shared__ uint32_t s_wsum[32];
 
   const int band = blockIdx.x;
@@ -114,92 +109,86 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_kernel(IntArgs a) {
   const int64_t px0 = (int64_t)band * BP;
   const int npx = (int)min((int64_t)BP, a.P - px0);
 
-  if (threadIdx.x == 0) {
-    const int64_t tfirst = a.ev[0].t_us;
-    s_flo = a.first_chunk ? 0 : lower_bound_i64(a.tf, a.F, tfirst);
-    s_fhi = a.ev_next ? lower_bound_i64(a.tf, a.F, a.ev_next->t_us) : a.F;
-    s_active = tfirst <= a.t_cap;
-    s_tbase = tfirst;
-    s_wide = (a.ev[a.n - 1].t_us - tfirst) > (int64_t)0xFFFFFFFFLL;
-  }
-  __syncthreads();
-  const int f_lo = s_flo, f_hi = s_fhi;
-  const bool active = s_active;
+  const ChunkInfo ci = *a.info;
+  const int f_lo = ci.f_lo, f_hi = ci.f_hi;
+  const bool active = ci.active != 0;
   if (!active && f_lo >= f_hi) return;
+  const bool wide = ci.wide != 0;
+  const int64_t tbase = ci.tbase;
+  const int n_tiles = a.n_tiles;
 
   for (int i = threadIdx.x; i < BP; i += NT) {
     const bool in = i < npx;
-    c.Ssm[i] = in ? a.S[px0 + i] : 0.f;
+    c.Ssm[i] = in ? (double)a.S[px0 + i] : 0.0;
     c.Tsm[i] = in ? a.T[px0 + i] : 0;
     c.tag[i] = 32;
   }
   int n_b = 0;
   if (active) {
-    // exclusive prefix of this band's per-tile counts -> pre[0..n_tiles]
-    uint32_t carry = 0;
-    for (int t0 = 0; t0 < a.n_tiles; t0 += NT) {
-      const int t = t0 + threadIdx.x;
-      const uint32_t cnt = t < a.n_tiles ? (a.meta[(int64_t)band * a.n_tiles + t] >> 16) : 0u;
-      uint32_t x = cnt;
+    for (int t = threadIdx.x; t < n_tiles; t += NT) c.mt[t] = a.meta[(int64_t)band * n_tiles + t];
+    __syncthreads();
+    // exclusive prefix of the per-tile counts: thread i owns tiles [i*per, (i+1)*per)
+    const int per = (n_tiles + NT - 1) / NT;
+    const int t0 = threadIdx.x * per;
+    uint32_t local = 0;
+    for (int t = t0; t < min(n_tiles, t0 + per); ++t) local += c.mt[t] >> 16;
+    uint32_t x = local;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) s_wsum[warp] = x;
-      __syncthreads();
-      uint32_t wpre = 0, tot = 0;
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t v = s_wsum[w];
-        if (w < warp) wpre += v;
-        tot += v;
-      }
-      if (t < a.n_tiles) c.pre[t] = carry + wpre + x - cnt;
-      carry += tot;
-      __syncthreads();
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
     }
-    if (threadIdx.x == 0) c.pre[a.n_tiles] = carry;
-    n_b = (int)carry;
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    uint32_t run = x - local, tot = 0;
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t v = s_wsum[w];
+      if (w < warp) run += v;
+      tot += v;
+    }
+    for (int t = t0; t < min(n_tiles, t0 + per); ++t) {
+      c.pre[t] = run;
+      run += c.mt[t] >> 16;
+    }
+    if (threadIdx.x == 0) c.pre[n_tiles] = tot;
+    n_b = (int)tot;
   }
   __syncthreads();
 
-  const bool wide = s_wide;
-  const int64_t tbase = s_tbase;
-  const float C = a.mp.C;
+  const double C = a.wp.C;
   int j = f_lo;
   bool done = false;
 
   for (int sb0 = 0; sb0 < n_b; sb0 += kSubBatch) {
     const int n_sb = min(kSubBatch, n_b - sb0);
-    // 1. gather the sub-batch (tile order = arrival order)
-    int tstart;
-    {
-      int lo = 0, hi = a.n_tiles;  // largest t with pre[t] <= sb0
+    const int n_ext = n_sb + (sb0 + n_sb < n_b ? 1 : 0);   // + first event of the next sub-batch
+    // 1. gather (arrival order): every position finds its tile by binary search in pre[]
+    for (int qq = threadIdx.x; qq < n_ext; qq += NT) {
+      const uint32_t q = (uint32_t)(sb0 + qq);
+      int lo = 0, hi = n_tiles;   // largest t with pre[t] <= q
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (c.pre[mid] <= (uint32_t)sb0) lo = mid; else hi = mid;
+        if (c.pre[mid] <= q) lo = mid; else hi = mid;
       }
-      tstart = lo;
-    }
-    for (int t = tstart + warp; t < a.n_tiles && c.pre[t] < (uint32_t)(sb0 + n_sb); t += NW) {
-      const int q0 = max((int)c.pre[t], sb0);
-      const int q1 = min((int)c.pre[t + 1], sb0 + n_sb);
-      if (q0 >= q1) continue;
-      const uint32_t m = a.meta[(int64_t)band * a.n_tiles + t];
-      const int64_t rbase = (int64_t)t * kTile + (m & 0xffffu) - c.pre[t];
-      bool twide = false;
-      int64_t t0 = tbase;
-      if (wide) { twide = a.tile_wide[t]; t0 = a.tile_t0[t]; }
-      for (int q = q0 + lane; q < q1; q += 32) {
-        const uint2 r = a.rec[rbase + q];
-        const int64_t tt = twide ? a.wide_t[rbase + q] : t0 + (int64_t)(uint32_t)(r.x - (uint32_t)t0);
-        c.At[q - sb0] = tt;
-        c.Apr[q - sb0] = r.y;
+      const int64_t idx = (int64_t)lo * kTile + (c.mt[lo] & 0xffffu) + (q - c.pre[lo]);
+      const uint2 r = a.rec[idx];
+      int64_t tt;
+      if (!wide) {
+        tt = tbase + (int64_t)(uint32_t)(r.x - (uint32_t)tbase);
+      } else if (a.tile_wide[lo]) {
+        tt = a.wide_t[idx];
+      } else {
+        const int64_t tb = a.tile_t0[lo];
+        tt = tb + (int64_t)(uint32_t)(r.x - (uint32_t)tb);
+      }
+      if (qq < n_sb) {
+        c.At[qq] = tt;
+        c.Apr[qq] = r.y;
+      } else {
+        s_tnext = tt;
       }
     }
-    if (threadIdx.x == 0)
-      s_tnext = (sb0 + kSubBatch < n_b) ? band_event_time(a, c.pre, band, sb0 + kSubBatch, wide, tbase)
-                                        : INT64_MAX;
+    if (n_ext == n_sb && threadIdx.x == 0) s_tnext = INT64_MAX;
     __syncthreads();
     const int64_t tnext = s_tnext;
 
@@ -239,9 +228,9 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_kernel(IntArgs a) {
           __syncwarp();
           if (win) {
             // Alg. 2 loop body
-            float s = c.Ssm[px] + (((int32_t)pr < 0) ? -C : C);     // S <- S + p C
-            s *= esi_decay(te - c.Tsm[px], a.dp);                     // S <- S * d(t - T)
-            c.Ssm[px] = fminf(fmaxf(s, a.mp.smin), a.mp.smax);        // clamp (Eq. 13)
+            double s = c.Ssm[px] + (((int32_t)pr < 0) ? -C : C);    // S <- S + p C
+            s *= wide_decay(te - c.Tsm[px], a.wp);                    // S <- S * d(t - T)
+            c.Ssm[px] = fmin(fmax(s, a.wp.smin), a.wp.smax);          // clamp (Eq. 13)
             c.Tsm[px] = te;                                           // T <- t
             c.tag[px] = 32;
             pend = false;
@@ -273,7 +262,7 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_kernel(IntArgs a) {
   if (n_b > 0) {
     __syncthreads();
     for (int i = threadIdx.x; i < npx; i += NT) {
-      a.S[px0 + i] = c.Ssm[i];
+      a.S[px0 + i] = (float)c.Ssm[i];
       a.T[px0 + i] = c.Tsm[i];
     }
   }
@@ -284,12 +273,12 @@ static cudaError_t launch_nw(const IntArgs& a, cudaStream_t s) {
   const size_t smem = integrate_smem_bytes(NW * kWarpPx);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(esi_integrate_kernel<NW>,
+    cudaError_t e = cudaFuncSetAttribute(esi_integrate_wide_kernel<NW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  esi_integrate_kernel<NW><<<a.nb, NW * 32, smem, s>>>(a);
+  esi_integrate_wide_kernel<NW><<<a.nb, NW * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 

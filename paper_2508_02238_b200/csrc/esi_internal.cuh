@@ -49,6 +49,15 @@ struct MapParams {
   int32_t readout_decay;
 };
 
+// fp64 copies of the parameters for the general (wide) K2 variant, which keeps S
+// in fp64 within a chunk (the fallback for spans >= 2^30 us and slow decays,
+// where fp32 rounding would accumulate over many barely-decayed events).
+struct WideParams {
+  double C, k_us, b, smin, smax, scale, off5;
+  int64_t dt_cut;
+  int32_t bmode, readout_decay;
+};
+
 struct PartArgs {
   const esi_event_t* ev;     // this chunk's events
   int64_t n;                 // events in the chunk
@@ -67,17 +76,26 @@ struct PartArgs {
   unsigned long long* err;
 };
 
+// Per-chunk facts computed once by esi_plan_kernel (one thread per chunk).
+struct ChunkInfo {
+  int64_t tbase;        // t of the chunk's first event
+  int64_t trel;         // base of the 32-bit relative times of the fast kernel:
+                        // min(first event, first frame rendered by the chunk)
+  int32_t f_lo, f_hi;   // frames rendered by this chunk: [f_lo, f_hi)
+  int32_t active;       // first event <= t_cap
+  int32_t wide;         // chunk spans >= 2^32 us (per-tile time bases needed)
+  int32_t fast;         // every relevant time within 2^30 us of trel: fast kernel applies
+  int32_t _pad;
+};
+
 struct IntArgs {
+  const ChunkInfo* info;             // this chunk's entry
   const uint2* rec;
   const uint32_t* meta;
   const int64_t* tile_t0;
   const int32_t* tile_wide;
   const int64_t* wide_t;
   int32_t n_tiles;
-  int32_t first_chunk;
-  int64_t n;                         // events in the chunk
-  const esi_event_t* ev;             // chunk events (first/last t)
-  const esi_event_t* ev_next;        // first event of the next chunk or nullptr
   const int64_t* tf;                 // frame times (device)
   int32_t F;
   int64_t t_cap;
@@ -89,6 +107,7 @@ struct IntArgs {
   int32_t vec8;                      // 8-byte frame stores allowed
   DecayParams dp;
   MapParams mp;
+  WideParams wp;
 };
 
 struct ReadoutArgs {
@@ -105,12 +124,16 @@ struct ReadoutArgs {
 
 size_t partition_smem_bytes(int nb);
 size_t integrate_smem_bytes(int band_px);
-cudaError_t launch_partition(const PartArgs& a, int n_tiles, cudaStream_t s);
+cudaError_t launch_partition(const PartArgs& a, int n_tiles, bool atomic_rank, cudaStream_t s);
+cudaError_t probe_atomic_order(unsigned* d_bad, cudaStream_t s);
 cudaError_t launch_integrate(const IntArgs& a, cudaStream_t s);
 cudaError_t launch_readout(const ReadoutArgs& a, cudaStream_t s);
-// plan: active[c] = 1 if chunk c's first event has t <= t_cap; count into *n_active
-cudaError_t launch_plan(const esi_event_t* const* chunk_first, int n_chunks, int64_t t_cap,
+// plan: ChunkInfo of every chunk and the number of chunks whose first event has t <= t_cap
+cudaError_t launch_plan(const esi_event_t* const* chunk_first, const int64_t* chunk_n, int n_chunks,
+                        const int64_t* tf, int F, int64_t t_cap, int allow_fast, ChunkInfo* info,
                         int32_t* n_active, cudaStream_t s);
+// fast kernel (32-bit relative times, dt_cut < 2^23) -- esi_integrate_fast.cu
+cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s);
 // consume: for segment k, count events with t <= t_cap (binary search), and set
 // *last_t to the t of the last consumed event of the last segment with one.
 cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,

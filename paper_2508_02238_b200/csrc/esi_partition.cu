@@ -55,6 +55,11 @@ __device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
   if (tid == 0) v[n] = wsum[32 + kPartThreads / 32 - 1];
 }
 
+// RANK_ATOMIC: per-warp rank from a shared-memory atomicAdd on the warp's private
+// (u16-packed) histogram -- relies on same-address lanes being served in lane
+// order, which esi_probe_atomic_order checks at esi_create; otherwise ranks come
+// from a ballot multi-split over the band bits (order by construction).
+template <bool RANK_ATOMIC>
 __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int nbp = (a.nb + 1) & ~1;
@@ -114,22 +119,32 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
       const uint32_t pid = y * (uint32_t)a.W + x;
       const uint32_t band = act ? (pid >> a.band_shift) : 0u;
       rec[r] = make_uint2((uint32_t)t, (pid & band_mask) | (p < 0 ? 0x80000000u : 0u));
-      // warp multi-split: lanes whose band equals mine
-      unsigned peers = __ballot_sync(kFull, act);
-      for (int bit = 0; bit < a.nb_bits; ++bit) {
-        const bool bset = (band >> bit) & 1u;
-        const unsigned bb = __ballot_sync(kFull, bset);
-        peers &= bset ? bb : ~bb;
+      uint32_t base, rank;
+      if (RANK_ATOMIC) {
+        uint32_t* hw = reinterpret_cast<uint32_t*>(myhist);
+        const uint32_t sh = (band & 1u) << 4;
+        const uint32_t old = act ? atomicAdd(hw + (band >> 1), 1u << sh) : 0u;
+        base = (old >> sh) & 0xffffu;
+        rank = 0;
+      } else {
+        // warp multi-split: lanes whose band equals mine
+        unsigned peers = __ballot_sync(kFull, act);
+#pragma unroll
+        for (int bit = 0; bit < 10; ++bit) {   // nb <= 1024: bits above nb_bits are 0 in every lane
+          const bool bset = (band >> bit) & 1u;
+          const unsigned bb = __ballot_sync(kFull, bset);
+          peers &= bset ? bb : ~bb;
+        }
+        if (!act) peers = 0u;
+        rank = __popc(peers & lanemask_lt());
+        base = 0;
+        if (act && rank == 0) {
+          base = myhist[band];
+          myhist[band] = (uint16_t)(base + __popc(peers));
+        }
+        base = __shfl_sync(kFull, base, act ? (__ffs(peers) - 1) : lane);
+        __syncwarp();
       }
-      if (!act) peers = 0u;
-      const unsigned rank = __popc(peers & lanemask_lt());
-      uint32_t base = 0;
-      if (act && rank == 0) {
-        base = myhist[band];
-        myhist[band] = (uint16_t)(base + __popc(peers));
-      }
-      base = __shfl_sync(kFull, base, act ? (__ffs(peers) - 1) : lane);
-      __syncwarp();
       rk[r] = (base + rank) | (band << 16);
     }
   }
@@ -190,16 +205,52 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
   }
 }
 
-cudaError_t launch_partition(const PartArgs& a, int n_tiles, cudaStream_t s) {
+template <bool RA>
+static cudaError_t launch_part_t(const PartArgs& a, int n_tiles, cudaStream_t s) {
   const size_t smem = partition_smem_bytes(a.nb);
   static size_t configured = 0;
   if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel,
+    cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel<RA>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  esi_partition_kernel<<<n_tiles, kPartThreads, smem, s>>>(a);
+  esi_partition_kernel<RA><<<n_tiles, kPartThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_partition(const PartArgs& a, int n_tiles, bool atomic_rank, cudaStream_t s) {
+  return atomic_rank ? launch_part_t<true>(a, n_tiles, s) : launch_part_t<false>(a, n_tiles, s);
+}
+
+// Probe: do warp-wide shared-memory atomicAdds on one address return values in
+// ascending lane order?  (ballot-derived stable ranks vs atomic ranks, random keys)
+__global__ void esi_probe_atomic_order_kernel(unsigned* bad) {
+  __shared__ unsigned h[4][512];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = lane; i < 512; i += 32) h[warp][i] = 0;
+  __syncwarp();
+  unsigned v = (blockIdx.x * 977u + threadIdx.x) * 2654435761u, nbad = 0;
+  for (int it = 0; it < 256; ++it) {
+    v = v * 1664525u + 1013904223u;
+    unsigned key = (v >> 9) & ((it & 3) == 0 ? 1u : ((it & 3) == 1 ? 15u : 511u));
+    unsigned peers = kFull;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+      const unsigned bb = __ballot_sync(kFull, (key >> b) & 1u);
+      peers &= ((key >> b) & 1u) ? bb : ~bb;
+    }
+    const unsigned before = h[warp][key];
+    __syncwarp();
+    const unsigned r = atomicAdd(&h[warp][key], 1u);
+    __syncwarp();
+    nbad += r != before + __popc(peers & lanemask_lt());
+  }
+  if (nbad) atomicAdd(bad, nbad);
+}
+
+cudaError_t probe_atomic_order(unsigned* d_bad, cudaStream_t s) {
+  esi_probe_atomic_order_kernel<<<148, 128, 0, s>>>(d_bad);
   return cudaGetLastError();
 }
 

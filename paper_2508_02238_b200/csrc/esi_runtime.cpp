@@ -66,6 +66,10 @@ struct esi_handle {
   size_t tf_cap = 0;
   const esi_event_t** d_chunk_first = nullptr;
   size_t cf_cap = 0;
+  int64_t* d_chunk_n = nullptr;
+  size_t cn_cap = 0;
+  ChunkInfo* d_info = nullptr;
+  size_t info_cap = 0;
   int64_t* d_cons = nullptr;
   size_t cons_cap = 0;
   unsigned long long* d_err = nullptr;
@@ -83,12 +87,15 @@ struct esi_handle {
   int64_t last_frame_t = INT64_MIN;
   DecayParams dp{};
   MapParams mp{};
+  WideParams wp{};
   bool timing = false;
   double kt_ms[4] = {0, 0, 0, 0};
   int64_t kt_n[4] = {0, 0, 0, 0};
   std::vector<TimedLaunch> timed;
   std::vector<cudaEvent_t> ev_pool;
-  int64_t st_launches = 0, st_events = 0, st_chunks = 0;
+  int64_t st_launches = 0, st_events = 0, st_chunks = 0, st_fast = 0;
+  bool atomic_rank = true;   // K1 ranks from lane-ordered smem atomics (probed at create)
+  bool allow_fast = true;    // K2 fast variant allowed (dt_cut < 2^23)
 };
 
 namespace {
@@ -241,6 +248,16 @@ void derive_params(esi_handle_t* h) {
   h->mp.off_int = (int32_t)std::floor(off);
   h->mp.off_frac = (float)(off - std::floor(off));
   h->mp.readout_decay = p.readout_decay ? 1 : 0;
+  h->wp.C = p.C;
+  h->wp.k_us = kk;
+  h->wp.b = p.b;
+  h->wp.smin = p.s_min;
+  h->wp.smax = p.s_max;
+  h->wp.scale = 255.0 / range;
+  h->wp.off5 = -p.s_min * 255.0 / range + 0.5;
+  h->wp.dt_cut = h->dp.dt_cut;
+  h->wp.bmode = h->dp.bmode;
+  h->wp.readout_decay = h->mp.readout_decay;
 }
 
 }  // namespace
@@ -329,6 +346,25 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   dalloc((void**)&h->d_n_active, sizeof(int32_t));
   if (!rc) rc = ensure_pinned(h, 1 << 16);
   if (!rc) rc = esi_reset(h);
+  h->allow_fast = h->dp.dt_cut < ((int64_t)1 << 23) && !getenv("ESI_DISABLE_FAST");
+  if (!rc) {
+    // K1 rank mode: probe that warp-wide smem atomics serve same-address lanes in lane order
+    const char* mode = getenv("ESI_RANK_MODE");
+    unsigned* d_bad = nullptr;
+    unsigned h_bad = 1;
+    if (cudaMalloc((void**)&d_bad, sizeof(unsigned)) == cudaSuccess &&
+        cudaMemsetAsync(d_bad, 0, sizeof(unsigned), h->stream) == cudaSuccess &&
+        probe_atomic_order(d_bad, h->stream) == cudaSuccess &&
+        cudaMemcpyAsync(&h_bad, d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream) == cudaSuccess &&
+        cudaStreamSynchronize(h->stream) == cudaSuccess) {
+      h->atomic_rank = (h_bad == 0);
+    } else {
+      cudaGetLastError();
+      h->atomic_rank = false;
+    }
+    if (d_bad) cudaFree(d_bad);
+    if (mode && strcmp(mode, "ballot") == 0) h->atomic_rank = false;
+  }
   if (!rc && cudaStreamSynchronize(h->stream) != cudaSuccess) rc = ESI_ERR_CUDA;
   if (rc) {
     esi_destroy(h);
@@ -347,7 +383,7 @@ void esi_destroy(esi_handle_t* h) {
   for (auto& tl : h->timed) { cudaEventDestroy(tl.a); cudaEventDestroy(tl.b); }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   void* bufs[] = {h->dS, h->dT, h->rec, h->meta, h->tile_t0, h->tile_wide, h->wide_t, h->d_tf,
-                  (void*)h->d_chunk_first, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames};
+                  (void*)h->d_chunk_first, h->d_chunk_n, h->d_info, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_pin) cudaFreeHost(h->h_pin);
@@ -441,6 +477,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
   h->st_launches = 0;
   h->st_events = 0;
   h->st_chunks = 0;
+  h->st_fast = 0;
 
   // frame times -> device
   int rc = ensure_dev(h, &h->d_tf, &h->tf_cap, F);
@@ -480,16 +517,26 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     timed_end(h, &tl);
     h->st_launches = 1;
   } else {
-    rc = ensure_dev(h, &h->d_chunk_first, &h->cf_cap, chunks.size());
-    if (rc) return rc;
-    rc = ensure_pinned(h, chunks.size() * sizeof(void*) + h->segs.size() * sizeof(int64_t) + 128);
+    const size_t nc = chunks.size();
+    rc = ensure_dev(h, &h->d_chunk_first, &h->cf_cap, nc);
+    if (!rc) rc = ensure_dev(h, &h->d_chunk_n, &h->cn_cap, nc);
+    if (!rc) rc = ensure_dev(h, &h->d_info, &h->info_cap, nc);
+    if (!rc) rc = ensure_pinned(h, nc * 16 + h->segs.size() * sizeof(int64_t) + 128);
     if (rc) return rc;
     const esi_event_t** hcf = (const esi_event_t**)h->h_pin;
-    for (size_t c = 0; c < chunks.size(); ++c) hcf[c] = chunks[c].ptr;
-    ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_first, hcf, chunks.size() * sizeof(void*), cudaMemcpyHostToDevice, st));
-    ESI_CUDA(h, launch_plan(h->d_chunk_first, (int)chunks.size(), t_cap, h->d_n_active, st));
-    int32_t* hna = (int32_t*)(h->h_pin + chunks.size() * sizeof(void*) + 16);
+    int64_t* hcn = (int64_t*)(h->h_pin + nc * sizeof(void*));
+    for (size_t c = 0; c < nc; ++c) {
+      hcf[c] = chunks[c].ptr;
+      hcn[c] = chunks[c].n;
+    }
+    ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_first, hcf, nc * sizeof(void*), cudaMemcpyHostToDevice, st));
+    ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_n, hcn, nc * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    ESI_CUDA(h, launch_plan(h->d_chunk_first, h->d_chunk_n, (int)nc, h->d_tf, (int)F, t_cap,
+                            h->allow_fast ? 1 : 0, h->d_info, h->d_n_active, st));
+    int32_t* hna = (int32_t*)(h->h_pin + nc * 16 + 16);
     ESI_CUDA(h, cudaMemcpyAsync(hna, h->d_n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    std::vector<ChunkInfo> hinfo(nc);
+    ESI_CUDA(h, cudaMemcpyAsync(hinfo.data(), h->d_info, nc * sizeof(ChunkInfo), cudaMemcpyDeviceToHost, st));
     ESI_CUDA(h, cudaStreamSynchronize(st));
     const int n_act = std::max(1, *hna);
     ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
@@ -519,20 +566,17 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.err = h->d_err;
       TimedLaunch t1;
       timed_begin(h, 0, &t1);
-      ESI_CUDA(h, launch_partition(pa, n_tiles, st));
+      ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, st));
       timed_end(h, &t1);
 
       IntArgs ia;
+      ia.info = h->d_info + c;
       ia.rec = h->rec;
       ia.meta = h->meta;
       ia.tile_t0 = h->tile_t0;
       ia.tile_wide = h->tile_wide;
       ia.wide_t = h->wide_t;
       ia.n_tiles = n_tiles;
-      ia.first_chunk = (c == 0);
-      ia.n = ch.n;
-      ia.ev = ch.ptr;
-      ia.ev_next = (c + 1 < (int)chunks.size()) ? chunks[c + 1].ptr : nullptr;
       ia.tf = h->d_tf;
       ia.F = (int32_t)F;
       ia.t_cap = t_cap;
@@ -545,9 +589,15 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       ia.vec8 = vec8;
       ia.dp = h->dp;
       ia.mp = h->mp;
+      ia.wp = h->wp;
       TimedLaunch t2;
       timed_begin(h, 1, &t2);
-      ESI_CUDA(h, launch_integrate(ia, st));
+      if (hinfo[c].fast) {
+        ESI_CUDA(h, launch_integrate_fast(ia, st));
+        h->st_fast += 1;
+      } else {
+        ESI_CUDA(h, launch_integrate(ia, st));
+      }
       timed_end(h, &t2);
       h->st_launches += 2;
       h->st_chunks += 1;
@@ -670,7 +720,7 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   pa.wide_t = h->wide_t;
   pa.err = h->d_err;
   ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), h->stream));
-  ESI_CUDA(h, launch_partition(pa, n_tiles, h->stream));
+  ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, h->stream));
   std::vector<uint2> rec(n_tiles * (size_t)kTile);
   std::vector<uint32_t> meta((size_t)h->nb * n_tiles);
   std::vector<int64_t> t0(n_tiles), wt;

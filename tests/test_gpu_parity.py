@@ -80,8 +80,14 @@ def test_c3_hot_pixels():
     check(w.W, w.H, ev_np_of(w), w.t_frames, w.params)
 
 
+def test_c2_ballot_rank_mode(monkeypatch):
+    monkeypatch.setenv("ESI_RANK_MODE", "ballot")
+    w = wl("c2")
+    check(w.W, w.H, ev_np_of(w), w.t_frames, w.params, chunk_events=262144)
+
+
 @pytest.mark.parametrize("b", [2.0, 1.0, 2.5, 0.5, 3.0])
-@pytest.mark.parametrize("k", [10.0, 100.0])
+@pytest.mark.parametrize("k", [10.0, 100.0, 0.05])
 @pytest.mark.parametrize("rd", [1, 0])
 def test_parameter_matrix(b, k, rd):
     ev = random_stream(int(b * 10 + k + rd), 40, 30, 60_000, 600_000)
@@ -202,8 +208,11 @@ def test_t_origin_and_late_start():
     check(16, 16, ev, tf, DEF, t_origin=5_000_000_000 - 40_000)
 
 
-def test_partition_is_bit_exact_stable_grouping():
+@pytest.mark.parametrize("rank_mode", ["auto", "ballot"])
+def test_partition_is_bit_exact_stable_grouping(rank_mode, monkeypatch):
     from paper_2508_02238_b200 import Esi
+    if rank_mode == "ballot":
+        monkeypatch.setenv("ESI_RANK_MODE", "ballot")
     for (W, H, n) in [(64, 48, 100_000), (346, 260, 300_000), (1280, 720, 2_000_000)]:
         ev = random_stream(W, W, H, n, 1_000_000, cluster=False)
         e = Esi(W, H)
