@@ -123,6 +123,26 @@ int esi_get_error(esi_handle_t* h);
 void esi_destroy(esi_handle_t* h);
 const char* esi_strerror(int status);
 
+/* ---- multi-GPU row-band routing ----
+ *
+ * ESI has no spatial coupling: an event changes only its own pixel (Alg. 2,
+ * P:242-253), so one large sensor can be split into row bands integrated by
+ * independent handles (one per GPU, created with height = band rows).
+ * esi_route_bands stably partitions the n time-ordered events at DEVICE pointer
+ * `events` by band -- band b = rows [row_start[b], row_start[b+1]),
+ * row_start[0] = 0 < row_start[1] < ... < row_start[n_bands] = height,
+ * 1 <= n_bands <= 64 -- into the DEVICE buffer `out` (n records, caller-owned):
+ * band-major, arrival order kept within a band (= a stable sort by band), with
+ * y rebased to y - row_start[b].  counts (HOST, n_bands entries) receives the
+ * events per band.  Both buffers must be 16-byte aligned and live on `device`;
+ * n < 2^32.  Events with y >= height: ESI_ERR_OUT_OF_BOUNDS (out unspecified);
+ * x, p and t are validated later by the band handle.  Runs on the cudaStream_t
+ * `stream` (NULL = the legacy default stream) and synchronises it (counts are
+ * host values when the call returns). */
+int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t height,
+                    const int32_t* row_start, int32_t n_bands, esi_event_t* out, int64_t* counts,
+                    void* stream);
+
 /* ---- instrumentation (used by bench.py and the parity tests) -------------- */
 
 /* Per-kernel device time accumulated by the handle when timing is enabled

@@ -16,10 +16,13 @@
 //   2. after a block barrier each warp scatters the indices of its slice into
 //      the destination warps' lists at (earlier slices' counts + running rank):
 //      a stable NW-way split, so every list is in arrival order;
-//   3. each warp walks its list, applying events with lowest-lane-first
-//      rounds for pixels hit twice in one 32-event batch, and reads frame j
-//      out (fused Eq. 14, 8-byte streaming stores) before the first event
-//      later than t_j.
+//   3. each warp walks its list 32 events at a time and reads frame j out
+//      (fused Eq. 14, 8-byte streaming stores) before the first event later
+//      than t_j.  Per batch the density decides the path (__match_any_sync):
+//      every pixel hit once -> the Alg. 2 body applied directly (sparse path,
+//      bit-identical to sequential fp32); some pixel hit several times -> a
+//      warp-shuffle inclusive scan of the clamped affine maps along each
+//      pixel's chain (dense path, dense_batch_apply).
 #include "esi_device.cuh"
 
 namespace esi {
@@ -46,12 +49,64 @@ __device__ __forceinline__ uint32_t fast_map(float v, const MapParams& mp, float
   return __float_as_uint(__fadd_rd(x, magic_off));             // 2^23 + off_int + floor(x)
 }
 
+
+// Clamped affine map s -> clamp(a s + c, lo, hi) with a >= 0 (SURVEY section 0,
+// finding 1).  The Alg. 2 body of event i is the map
+// f_i = (d_i, d_i p_i C, S_min, S_max); such maps are closed under composition:
+//   F o G = (aF aG, aF cG + cF, clamp(aF loG + cF, loF, hiF), clamp(aF hiG + cF, loF, hiF)).
+// Dense batch (some pixel hit by several of the warp's 32 events): each lane
+// builds its event's map, then a pointer-jumping inclusive scan along the
+// per-pixel chains (previous event of the same pixel = highest lower peer lane
+// from __match_any_sync) composes every prefix in <= 5 shuffle rounds; lane i's
+// state is prefix_i applied to the pixel's state before the batch.  Pixels hit
+// once keep the direct Alg. 2 arithmetic (bit-identical to the sparse path).
+template <int BM>
+__device__ __forceinline__ void dense_batch_apply(float* S, int32_t* T, bool act, int px, unsigned peers,
+                                                  int32_t te, float pc, int lane, const DecayParams& dp,
+                                                  const MapParams& mp, int32_t dt_cut) {
+  const unsigned below = act ? (peers & lanemask_lt()) : 0u;
+  const int prev = below ? 31 - __clz(below) : -1;          // previous event of my pixel in the batch
+  const int32_t t_prev_lane = __shfl_sync(kFull, te, prev < 0 ? lane : prev);
+  float s0 = 0.f;
+  int32_t tp = t_prev_lane;
+  if (act) {
+    s0 = S[px];                                               // state before the batch
+    if (prev < 0) tp = T[px];
+  }
+  __syncwarp();                                               // all reads before any write
+  const float d = act ? fast_decay<BM>(te - tp, dp, dt_cut) : 1.f;
+  float fa = d, fc = d * pc, flo = mp.smin, fhi = mp.smax;    // f_i
+  int ptr = prev;
+  while (__any_sync(kFull, ptr >= 0)) {
+    const int src = ptr >= 0 ? ptr : lane;
+    const float ga = __shfl_sync(kFull, fa, src), gc = __shfl_sync(kFull, fc, src);
+    const float glo = __shfl_sync(kFull, flo, src), ghi = __shfl_sync(kFull, fhi, src);
+    const int gp = __shfl_sync(kFull, ptr, src);
+    if (ptr >= 0) {                                           // F <- F o G
+      const float nlo = fminf(fmaxf(fmaf(fa, glo, fc), flo), fhi);
+      const float nhi = fminf(fmaxf(fmaf(fa, ghi, fc), flo), fhi);
+      fc = fmaf(fa, gc, fc);
+      fa = fa * ga;
+      flo = nlo;
+      fhi = nhi;
+      ptr = gp;
+    }
+  }
+  const bool single = __popc(peers) == 1;
+  const float v = single ? fminf(fmaxf((s0 + pc) * d, mp.smin), mp.smax)   // direct Alg. 2 body
+                         : fminf(fmaxf(fmaf(fa, s0, fc), flo), fhi);       // prefix_i(s0)
+  const unsigned above = peers & ~lanemask_lt() & ~(1u << lane);
+  if (act && above == 0u) {                                   // last event of its pixel in the batch
+    S[px] = v;
+    T[px] = te;
+  }
+}
+
 template <int NW>
 struct FastSmem {
   static constexpr int BP = NW * kWarpPx;
   float S[BP];
   int32_t T[BP];
-  int32_t tag[BP];
   int32_t At[kSubBatch];
   uint32_t Apr[kSubBatch];
   uint32_t pre[kMaxTilesPerChunk + 1];
@@ -122,7 +177,6 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_kernel(IntArgs a) {
     const bool in = i < npx;
     sm.S[i] = in ? a.S[px0 + i] : 0.f;
     sm.T[i] = in ? (int32_t)max(a.T[px0 + i] - trel, (int64_t)t_clamp) : t_clamp;
-    sm.tag[i] = 32;
   }
   int n_b = 0;
   if (active) {
@@ -244,24 +298,24 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_kernel(IntArgs a) {
       const bool valid = lane < m && te <= tj;
       const int nv = __popc(__ballot_sync(kFull, valid));
       if (nv > 0) {
-        bool pend = lane < nv;
+        const bool act = lane < nv;
         const int px = (int)(pr & (uint32_t)(BP - 1));
-        do {
-          if (pend) atomicMin(&sm.tag[px], lane);
-          __syncwarp();
-          const bool win = pend && sm.tag[px] == lane;
-          __syncwarp();
-          if (win) {
-            // Alg. 2 loop body
-            float s = sm.S[px] + (((int32_t)pr < 0) ? -C : C);            // S <- S + p C
+        // lanes of this batch that hit the same pixel (inactive lanes: singleton keys)
+        const unsigned peers = __match_any_sync(kFull, act ? px : BP + lane);
+        const float pc = ((int32_t)pr < 0) ? -C : C;
+        if (!__any_sync(kFull, act && __popc(peers) > 1)) {
+          // sparse batch: every pixel hit once -> Alg. 2 body applied directly,
+          // bit-identical to a sequential fp32 evaluation
+          if (act) {
+            float s = sm.S[px] + pc;                                      // S <- S + p C
             s *= fast_decay<BM>(te - sm.T[px], a.dp, dt_cut);             // S <- S d(t - T)
             sm.S[px] = fminf(fmaxf(s, a.mp.smin), a.mp.smax);             // clamp (Eq. 13)
             sm.T[px] = te;                                                // T <- t
-            sm.tag[px] = 32;
-            pend = false;
           }
-          __syncwarp();
-        } while (__any_sync(kFull, pend));
+        } else {
+          dense_batch_apply<BM>(sm.S, sm.T, act, px, peers, te, pc, lane, a.dp, a.mp, dt_cut);
+        }
+        __syncwarp();
       }
       i += nv;
       if (nv < m) {

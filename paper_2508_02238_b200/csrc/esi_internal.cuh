@@ -122,6 +122,11 @@ struct ReadoutArgs {
   MapParams mp;
 };
 
+// Row bands of esi_route_bands: band b = rows [start[b], start[b+1]).
+struct RouteRows {
+  int32_t start[65];
+};
+
 size_t partition_smem_bytes(int nb);
 size_t integrate_smem_bytes(int band_px);
 cudaError_t launch_partition(const PartArgs& a, int n_tiles, bool atomic_rank, cudaStream_t s);
@@ -138,6 +143,11 @@ cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s);
 // *last_t to the t of the last consumed event of the last segment with one.
 cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,
                            int64_t* last_t, cudaStream_t s);
+// row-band routing (esi_route.cu): hist + scan + stable scatter on stream s
+cudaError_t launch_route(const esi_event_t* ev, int64_t n, int32_t H, int nb, const RouteRows& rr,
+                         uint32_t* tile_cnt, int64_t* band_tot, esi_event_t* out,
+                         unsigned long long* err, cudaStream_t s);
+int64_t route_tiles(int64_t n);
 cudaError_t launch_fill_i64(int64_t* p, int64_t n, int64_t v, cudaStream_t s);
 cudaError_t launch_validate(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
                             int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,

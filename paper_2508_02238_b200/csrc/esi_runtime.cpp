@@ -685,6 +685,49 @@ int esi_last_render_stats(esi_handle_t* h, int64_t* launches, int64_t* events, i
   return ESI_OK;
 }
 
+int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t height,
+                    const int32_t* row_start, int32_t n_bands, esi_event_t* out, int64_t* counts,
+                    void* stream) {
+  if (!row_start || !counts || n_bands < 1 || n_bands > 64 || height < 1) return ESI_ERR_INVALID_ARG;
+  if (row_start[0] != 0 || row_start[n_bands] != height) return ESI_ERR_INVALID_ARG;
+  for (int b = 0; b < n_bands; ++b)
+    if (row_start[b + 1] <= row_start[b]) return ESI_ERR_INVALID_ARG;
+  if (n == 0) {
+    for (int b = 0; b < n_bands; ++b) counts[b] = 0;
+    return ESI_OK;
+  }
+  if (!events || !out || ((uintptr_t)events & 15) || ((uintptr_t)out & 15) || n >= ((size_t)1 << 32))
+    return ESI_ERR_INVALID_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_INVALID_ARG; }
+  if (!is_device_ptr(events) || !is_device_ptr(out)) return ESI_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  RouteRows rr;
+  for (int b = 0; b <= 64; ++b) rr.start[b] = b <= n_bands ? row_start[b] : height;
+  const int64_t n_tiles = route_tiles((int64_t)n);
+  uint32_t* tile_cnt = nullptr;
+  int64_t* band_tot = nullptr;
+  unsigned long long* err = nullptr;
+  const size_t bytes = (size_t)n_bands * n_tiles * sizeof(uint32_t) + 64 * sizeof(int64_t) + 16;
+  unsigned char* scratch = nullptr;
+  if (cudaMallocAsync((void**)&scratch, bytes, st) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_OOM; }
+  band_tot = (int64_t*)scratch;
+  err = (unsigned long long*)(scratch + 64 * sizeof(int64_t));
+  tile_cnt = (uint32_t*)(scratch + 64 * sizeof(int64_t) + 16);
+  int rc = ESI_OK;
+  unsigned long long herr = kNoError;
+  if (cudaMemsetAsync(err, 0xff, sizeof(*err), st) != cudaSuccess ||
+      launch_route(events, (int64_t)n, height, n_bands, rr, tile_cnt, band_tot, out, err, st) != cudaSuccess ||
+      cudaMemcpyAsync(counts, band_tot, n_bands * sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&herr, err, sizeof(herr), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaFreeAsync(scratch, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+    if (getenv("ESI_DEBUG")) fprintf(stderr, "[esi] route: %s\n", cudaGetErrorString(cudaGetLastError()));
+    cudaGetLastError();
+    return ESI_ERR_CUDA;
+  }
+  if (herr != kNoError) rc = (int)(herr & 0xff);
+  return rc;
+}
+
 int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8_t* out_p,
                         size_t n_out, uint32_t* band_start, int32_t* nb_out, int32_t* band_px_out) {
   if (!h || !band_start || !nb_out || !band_px_out) return ESI_ERR_INVALID_ARG;
