@@ -105,8 +105,12 @@ int esi_push_events(esi_handle_t* h, const esi_event_t* events, size_t n);
 int esi_render(esi_handle_t* h, int64_t t_frame_us, uint8_t* out);
 
 /* Renders n frames at the non-decreasing host array t_frames_us[0..n) into
- * out[n][height][width] (host or device).  Bit-identical to n esi_render
- * calls.  Events with t > t_frames_us[n-1] stay pending.  Synchronous. */
+ * out[n][height][width] (host or device).  Equivalent to n esi_render calls:
+ * bit-identical for every pixel that never receives two events inside one
+ * 32-event integration batch (the sparse path); pixels integrated by the dense
+ * warp-scan path (reassociated clamped-affine composition)
+ * agree within the fp32 state tolerance.  Events with t > t_frames_us[n-1]
+ * stay pending.  Synchronous. */
 int esi_render_many(esi_handle_t* h, const int64_t* t_frames_us, size_t n, uint8_t* out);
 
 /* Copies the state out (host pointers, width*height each; either may be NULL).

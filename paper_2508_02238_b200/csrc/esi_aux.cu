@@ -66,7 +66,7 @@ __global__ void esi_plan_kernel(const esi_event_t* const* chunk_first, const int
       hi = max(hi, tf[ci.f_hi - 1]);
     }
     ci.trel = lo;
-    ci.fast = allow_fast && (hi - lo) < ((int64_t)1 << 30);
+    ci.fast = allow_fast && (hi - lo) < ((int64_t)1 << 24);   // fp32-exact relative times
     ci._pad = 0;
     info[c] = ci;
     // first events are non-decreasing: the active chunks are a prefix

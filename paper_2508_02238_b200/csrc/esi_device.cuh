@@ -21,6 +21,11 @@ __device__ __forceinline__ void st_stream8(void* p, uint32_t lo, uint32_t hi) {
   asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(lo), "r"(hi) : "memory");
 }
 
+// 4-byte streaming store of frame bytes.
+__device__ __forceinline__ void st_stream4(void* p, uint32_t v) {
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Eq. 4: d(dt) = max{(1 - k dt)^b, 0}, dt in integer microseconds (>= 0).
 // u = 1 - k dt is formed with a float pair (kh + kl = k * 1e-6) so that u keeps
 // ~1 ulp relative accuracy near the cutoff (SURVEY 8(c) numerics); dt >= dt_cut

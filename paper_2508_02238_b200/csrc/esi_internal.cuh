@@ -37,6 +37,8 @@ struct DecayParams {
   int32_t use_f64;
   int32_t bmode;         // 1,2,3,4: integer b fast path; 0: exp2(b log2 u)
   float b;
+  // fast K2: u = kf * ((tau_h - dt) + tau_l) with tau = 1e6/k us = tau_h + tau_l
+  float tau_h, tau_l, kf;
 };
 
 struct MapParams {
@@ -45,6 +47,7 @@ struct MapParams {
   // Eq. 14 + 0.5 = v*scale + off, off = -smin*scale + 0.5 split as off_int + off_frac so
   // that a tiny |v| is not absorbed by the offset (v = -1e-9 must give 127, not 128).
   float scale, off_frac;
+  float scale_w2;        // (k * 1e-6)^2 * scale: folded b = 2 readout of the fast K2
   int32_t off_int;
   int32_t readout_decay;
 };

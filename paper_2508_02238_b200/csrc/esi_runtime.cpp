@@ -40,6 +40,7 @@ struct Chunk {
 struct TimedLaunch {
   int kind;
   cudaEvent_t a, b;
+  cudaStream_t s;
 };
 
 }  // namespace
@@ -55,12 +56,14 @@ struct esi_handle {
   float* dS = nullptr;
   int64_t* dT = nullptr;
   std::vector<Segment> segs;
-  // K1/K2 scratch
-  uint2* rec = nullptr;
-  uint32_t* meta = nullptr;
-  int64_t* tile_t0 = nullptr;
-  int32_t* tile_wide = nullptr;
-  int64_t* wide_t = nullptr;
+  // K1/K2 scratch, double-buffered: K1 of chunk c+1 (stream aux) overlaps K2 of chunk c
+  uint2* rec[2] = {nullptr, nullptr};
+  uint32_t* meta[2] = {nullptr, nullptr};
+  int64_t* tile_t0[2] = {nullptr, nullptr};
+  int32_t* tile_wide[2] = {nullptr, nullptr};
+  int64_t* wide_t[2] = {nullptr, nullptr};
+  cudaStream_t aux = nullptr;               // K1 stream
+  cudaEvent_t ev_k1[2] = {nullptr, nullptr}, ev_k2[2] = {nullptr, nullptr}, ev_start = nullptr;
   // small device buffers
   int64_t* d_tf = nullptr;
   size_t tf_cap = 0;
@@ -191,17 +194,18 @@ cudaEvent_t take_event(esi_handle_t* h) {
   return e;
 }
 
-void timed_begin(esi_handle_t* h, int kind, TimedLaunch* tl) {
+void timed_begin(esi_handle_t* h, int kind, TimedLaunch* tl, cudaStream_t s = nullptr) {
   if (!h->timing) return;
   tl->kind = kind;
   tl->a = take_event(h);
   tl->b = take_event(h);
-  cudaEventRecord(tl->a, h->stream);
+  tl->s = s ? s : h->stream;
+  cudaEventRecord(tl->a, tl->s);
 }
 
 void timed_end(esi_handle_t* h, TimedLaunch* tl) {
   if (!h->timing) return;
-  cudaEventRecord(tl->b, h->stream);
+  cudaEventRecord(tl->b, tl->s);
   h->timed.push_back(*tl);
 }
 
@@ -238,12 +242,16 @@ void derive_params(esi_handle_t* h) {
   h->dp.dt_cut = horizon >= 9.0e18 ? INT64_MAX : (int64_t)std::ceil(horizon);
   h->dp.use_f64 = h->dp.dt_cut > (int64_t)(1 << 24);
   h->dp.b = (float)p.b;
+  h->dp.tau_h = (float)horizon;
+  h->dp.tau_l = (float)(horizon - (double)h->dp.tau_h);
+  h->dp.kf = (float)kk;
   h->dp.bmode = (p.b == 1.0 || p.b == 2.0 || p.b == 3.0 || p.b == 4.0) ? (int)p.b : 0;
   h->mp.C = (float)p.C;
   h->mp.smin = (float)p.s_min;
   h->mp.smax = (float)p.s_max;
   const double range = p.s_max - p.s_min;
   h->mp.scale = (float)(255.0 / range);
+  h->mp.scale_w2 = (float)(kk * kk * 255.0 / range);
   const double off = -p.s_min * 255.0 / range + 0.5;
   h->mp.off_int = (int32_t)std::floor(off);
   h->mp.off_frac = (float)(off - std::floor(off));
@@ -314,8 +322,17 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   h->P = P;
   h->prm = prm;
   derive_params(h);
+  // Band size (K1 partition key, K2 CTA): the largest power-of-two multiple of
+  // 256 pixels that still gives >= 2 bands per SM (2 x 148), so that K2's
+  // (tile, band) segments are as long as possible without starving the grid;
+  // never more than kMaxBands bands (K1's shared-memory histograms).
   h->band_px = kWarpPx;
+  while (h->band_px < kMaxBandPx && (P + 2 * h->band_px - 1) / (2 * h->band_px) >= 296) h->band_px <<= 1;
   while ((P + h->band_px - 1) / h->band_px > kMaxBands) h->band_px <<= 1;
+  if (const char* bp = getenv("ESI_BAND_PX")) {
+    const int v = atoi(bp);
+    if (v >= kWarpPx && v <= kMaxBandPx && (v & (v - 1)) == 0 && (P + v - 1) / v <= kMaxBands) h->band_px = v;
+  }
   h->band_shift = 0;
   while ((1 << h->band_shift) < h->band_px) ++h->band_shift;
   h->nb = (int)((P + h->band_px - 1) / h->band_px);
@@ -336,11 +353,19 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   h->stream = h->own_stream;
   dalloc((void**)&h->dS, P * sizeof(float));
   dalloc((void**)&h->dT, P * sizeof(int64_t));
-  dalloc((void**)&h->rec, ce * sizeof(uint2));
-  dalloc((void**)&h->meta, (size_t)h->nb * h->max_tiles * sizeof(uint32_t));
-  dalloc((void**)&h->tile_t0, h->max_tiles * sizeof(int64_t));
-  dalloc((void**)&h->tile_wide, h->max_tiles * sizeof(int32_t));
-  dalloc((void**)&h->wide_t, ce * sizeof(int64_t));
+  for (int b = 0; b < 2; ++b) {
+    dalloc((void**)&h->rec[b], ce * sizeof(uint2));
+    dalloc((void**)&h->meta[b], (size_t)h->nb * h->max_tiles * sizeof(uint32_t));
+    dalloc((void**)&h->tile_t0[b], h->max_tiles * sizeof(int64_t));
+    dalloc((void**)&h->tile_wide[b], h->max_tiles * sizeof(int32_t));
+    dalloc((void**)&h->wide_t[b], ce * sizeof(int64_t));
+    if (!rc && (cudaEventCreateWithFlags(&h->ev_k1[b], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&h->ev_k2[b], cudaEventDisableTiming) != cudaSuccess))
+      rc = ESI_ERR_CUDA;
+  }
+  if (!rc && (cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
+              cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) != cudaSuccess))
+    rc = ESI_ERR_CUDA;
   dalloc((void**)&h->d_err, sizeof(unsigned long long));
   dalloc((void**)&h->d_last_t, sizeof(int64_t));
   dalloc((void**)&h->d_n_active, sizeof(int32_t));
@@ -382,10 +407,18 @@ void esi_destroy(esi_handle_t* h) {
   for (auto& p : h->pool) cudaFree(p.first);
   for (auto& tl : h->timed) { cudaEventDestroy(tl.a); cudaEventDestroy(tl.b); }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
-  void* bufs[] = {h->dS, h->dT, h->rec, h->meta, h->tile_t0, h->tile_wide, h->wide_t, h->d_tf,
+  if (h->aux) cudaStreamSynchronize(h->aux);
+  void* bufs[] = {h->dS, h->dT, h->rec[0], h->meta[0], h->tile_t0[0], h->tile_wide[0], h->wide_t[0],
+                  h->rec[1], h->meta[1], h->tile_t0[1], h->tile_wide[1], h->wide_t[1], h->d_tf,
                   (void*)h->d_chunk_first, h->d_chunk_n, h->d_info, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (int b = 0; b < 2; ++b) {
+    if (h->ev_k1[b]) cudaEventDestroy(h->ev_k1[b]);
+    if (h->ev_k2[b]) cudaEventDestroy(h->ev_k2[b]);
+  }
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
+  if (h->aux) cudaStreamDestroy(h->aux);
   if (h->h_pin) cudaFreeHost(h->h_pin);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   cudaGetLastError();
@@ -541,8 +574,14 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     const int n_act = std::max(1, *hna);
     ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
 
+    // K1 runs on the aux stream, K2 on the handle's stream; chunk c uses buffer c & 1:
+    // K1(c) waits for the render's setup and for K2(c-2); K2(c) waits for K1(c).
+    ESI_CUDA(h, cudaEventRecord(h->ev_start, st));
+    ESI_CUDA(h, cudaStreamWaitEvent(h->aux, h->ev_start, 0));
     int64_t index_base = 0;
     for (int c = 0; c < n_act; ++c) {
+      const int bf = c & 1;
+      if (c >= 2) ESI_CUDA(h, cudaStreamWaitEvent(h->aux, h->ev_k2[bf], 0));
       const Chunk& ch = chunks[c];
       const int n_tiles = (int)((ch.n + kTile - 1) / kTile);
       PartArgs pa;
@@ -558,24 +597,26 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.band_shift = h->band_shift;
       pa.nb = h->nb;
       pa.nb_bits = h->nb_bits;
-      pa.rec = h->rec;
-      pa.meta = h->meta;
-      pa.tile_t0 = h->tile_t0;
-      pa.tile_wide = h->tile_wide;
-      pa.wide_t = h->wide_t;
+      pa.rec = h->rec[bf];
+      pa.meta = h->meta[bf];
+      pa.tile_t0 = h->tile_t0[bf];
+      pa.tile_wide = h->tile_wide[bf];
+      pa.wide_t = h->wide_t[bf];
       pa.err = h->d_err;
       TimedLaunch t1;
-      timed_begin(h, 0, &t1);
-      ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, st));
+      timed_begin(h, 0, &t1, h->aux);
+      ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, h->aux));
       timed_end(h, &t1);
+      ESI_CUDA(h, cudaEventRecord(h->ev_k1[bf], h->aux));
+      ESI_CUDA(h, cudaStreamWaitEvent(st, h->ev_k1[bf], 0));
 
       IntArgs ia;
       ia.info = h->d_info + c;
-      ia.rec = h->rec;
-      ia.meta = h->meta;
-      ia.tile_t0 = h->tile_t0;
-      ia.tile_wide = h->tile_wide;
-      ia.wide_t = h->wide_t;
+      ia.rec = h->rec[bf];
+      ia.meta = h->meta[bf];
+      ia.tile_t0 = h->tile_t0[bf];
+      ia.tile_wide = h->tile_wide[bf];
+      ia.wide_t = h->wide_t[bf];
       ia.n_tiles = n_tiles;
       ia.tf = h->d_tf;
       ia.F = (int32_t)F;
@@ -599,6 +640,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
         ESI_CUDA(h, launch_integrate(ia, st));
       }
       timed_end(h, &t2);
+      ESI_CUDA(h, cudaEventRecord(h->ev_k2[bf], st));
       h->st_launches += 2;
       h->st_chunks += 1;
       index_base += ch.n;
@@ -756,11 +798,11 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   pa.band_shift = h->band_shift;
   pa.nb = h->nb;
   pa.nb_bits = h->nb_bits;
-  pa.rec = h->rec;
-  pa.meta = h->meta;
-  pa.tile_t0 = h->tile_t0;
-  pa.tile_wide = h->tile_wide;
-  pa.wide_t = h->wide_t;
+  pa.rec = h->rec[0];
+  pa.meta = h->meta[0];
+  pa.tile_t0 = h->tile_t0[0];
+  pa.tile_wide = h->tile_wide[0];
+  pa.wide_t = h->wide_t[0];
   pa.err = h->d_err;
   ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), h->stream));
   ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, h->stream));
@@ -768,16 +810,16 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   std::vector<uint32_t> meta((size_t)h->nb * n_tiles);
   std::vector<int64_t> t0(n_tiles), wt;
   std::vector<int32_t> wide(n_tiles);
-  ESI_CUDA(h, cudaMemcpyAsync(rec.data(), h->rec, n * sizeof(uint2), cudaMemcpyDeviceToHost, h->stream));
-  ESI_CUDA(h, cudaMemcpyAsync(meta.data(), h->meta, meta.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
-  ESI_CUDA(h, cudaMemcpyAsync(t0.data(), h->tile_t0, n_tiles * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
-  ESI_CUDA(h, cudaMemcpyAsync(wide.data(), h->tile_wide, n_tiles * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaMemcpyAsync(rec.data(), h->rec[0], n * sizeof(uint2), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaMemcpyAsync(meta.data(), h->meta[0], meta.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaMemcpyAsync(t0.data(), h->tile_t0[0], n_tiles * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  ESI_CUDA(h, cudaMemcpyAsync(wide.data(), h->tile_wide[0], n_tiles * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
   ESI_CUDA(h, cudaStreamSynchronize(h->stream));
   bool any_wide = false;
   for (int t = 0; t < n_tiles; ++t) any_wide |= wide[t] != 0;
   if (any_wide) {
     wt.resize(n);
-    ESI_CUDA(h, cudaMemcpy(wt.data(), h->wide_t, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    ESI_CUDA(h, cudaMemcpy(wt.data(), h->wide_t[0], n * sizeof(int64_t), cudaMemcpyDeviceToHost));
   }
   size_t o = 0;
   for (int b = 0; b < h->nb; ++b) {
