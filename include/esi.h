@@ -80,7 +80,7 @@ typedef struct esi_handle esi_handle_t;
 void esi_default_params(esi_params_t* p);
 
 /* Creates a handle for a width x height sensor (1 <= width, height <= 65535,
- * width*height <= 2^23).  Allocates the per-pixel state S (fp32) and T (int64)
+ * width*height <= 2^22 = 4194304).  Allocates the per-pixel state S (fp32) and T (int64)
  * on the device, S = 0, T = t_origin (Alg. 2 "Initialize").
  * Returns ESI_ERR_INVALID_ARG for bad sizes/params, ESI_ERR_OOM, ESI_ERR_CUDA. */
 int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_handle_t** out);

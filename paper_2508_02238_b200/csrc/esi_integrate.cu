@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
 
   const int band = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t px0 = (int64_t)band * BP;
-  const int npx = (int)min((int64_t)BP, a.P - px0);
+  const int64_t px0 = (int64_t)band * a.band_px;            // band_px <= BP
+  const int npx = (int)min((int64_t)a.band_px, a.P - px0);
 
   const ChunkInfo ci = *a.info;
   const int f_lo = ci.f_lo, f_hi = ci.f_hi;
@@ -283,14 +283,8 @@ static cudaError_t launch_nw(const IntArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_integrate(const IntArgs& a, cudaStream_t s) {
-  switch (a.band_px / kWarpPx) {
-    case 1: return launch_nw<1>(a, s);
-    case 2: return launch_nw<2>(a, s);
-    case 4: return launch_nw<4>(a, s);
-    case 8: return launch_nw<8>(a, s);
-    case 16: return launch_nw<16>(a, s);
-    default: return cudaErrorInvalidValue;
-  }
+  // 16 warps x 256 pixels cover any band (band_px <= kMaxBandPx = 4096)
+  return launch_nw<16>(a, s);
 }
 
 }  // namespace esi

@@ -1,29 +1,21 @@
 // esi_integrate_fast.cu -- K2: per-band integration (Alg. 2) fused
 // with the Eq. 13/14 readout of every frame of the chunk.
 //
-// One CTA per band of BP = NW*256 consecutive pixel ids (K1's partition key);
-// warp w owns the 256 pixels [w*256, w*256+256) of the band, lane l the 8
-// pixels [w*256 + 8l, +8).  The band's state lives in shared memory for the
-// whole chunk: S (fp32) and T as an fp32 offset from the chunk base
-// ChunkInfo::trel (exact integers: |T| < 2^24 us; pixels older than the decay
-// horizon are clamped to -(dt_cut+1), i.e. "fully decayed").
+// One CTA of 16 warps per band of band_px consecutive pixel ids (K1's
+// partition key; band_px is a run-time multiple of 64 chosen so that the grid
+// fills the SMs evenly).  The band's state lives in shared memory for the whole
+// chunk: S (fp32) and T as an fp32 offset from the chunk base ChunkInfo::trel
+// (exact integers: |T| < 2^24 us; pixels older than the decay horizon are
+// clamped to -(dt_cut+1), i.e. "fully decayed").
 //
-// Per sub-batch of SB = NW*256 band events (arrival order):
-//   1. gather: warps copy the band's (tile, band) segments written by K1 -- in
-//      tile order, i.e. arrival order -- into sub[] (one warp per segment);
-//   2. split: warp w takes slice w of sub[], ranks each event among the
-//      slice's events bound for the same owner warp (__match_any_sync), and
-//      after a block-wide scan of the NW x NW slice/owner counts scatters it to
-//      lst[] -- owner-major, arrival-order-minor (a stable NW-way split);
-//   3. walk: each warp walks its list 32 events at a time.  Before the first
-//      event later than frame time t_j it reads frame j out for its 256 pixels
-//      (fused Eq. 13 + Eq. 14, packed f32x2 arithmetic, 8-byte streaming
-//      stores).  Per batch, the density of the batch picks the path:
-//        sparse (every pixel hit once): the Alg. 2 body applied directly --
-//          bit-identical to a sequential fp32 evaluation;
-//        dense (some pixel hit several times): a warp-shuffle inclusive scan
-//          of the events' clamped affine maps along each pixel's chain
-//          (dense_batch_apply).
+// Per sub-batch of kSB band events (arrival order):
+//   1. gather: cp.async copies of the band's (tile, band) segments written by
+//      K1, in tile order = arrival order (double-buffered);
+//   2. segments = the events of one frame window inside the sub-batch; per
+//      segment: claim (atomicExch chains), apply (sparse / chain / dense
+//      paths, see process_segment), and at the window end the fused Eq. 13 +
+//      Eq. 14 readout of frame j for the band (packed f32x2 arithmetic,
+//      4-byte streaming stores).
 // Decay (Eq. 4, reading A14): with tau = 1e6/k us split as tau_h + tau_l,
 //   u = k_us * ((tau_h - dt) + tau_l),  d = max(u, 0)^b
 // (tau_h - dt is exact near the cutoff, so u keeps full relative precision and
@@ -90,55 +82,6 @@ __device__ __forceinline__ float ev_decay(float dt, const FastConst& c) {
 // Eq. 13 clamp of one event's result.
 __device__ __forceinline__ float clampS(float s, const FastConst& c) { return fminf(fmaxf(s, c.smin), c.smax); }
 
-// Clamped affine map s -> clamp(a s + c, lo, hi) with a >= 0 (SURVEY section 0,
-// finding 1).  The Alg. 2 body of event i is the map
-// f_i = (d_i, d_i p_i C, S_min, S_max); such maps are closed under composition:
-//   F o G = (aF aG, aF cG + cF, clamp(aF loG + cF, loF, hiF), clamp(aF hiG + cF, loF, hiF)).
-// Dense batch: each lane builds its event's map, then a pointer-jumping
-// inclusive scan along the per-pixel chains (previous event of the same pixel
-// = highest lower peer lane from __match_any_sync) composes every prefix in
-// <= 5 shuffle rounds; lane i's state is prefix_i applied to the pixel's state
-// before the batch.  Pixels hit once keep the direct Alg. 2 arithmetic.
-template <int BM>
-__device__ __forceinline__ void dense_batch_apply(float* S, float* T, bool act, int px, unsigned peers,
-                                                  float te, float pc, int lane, const FastConst& k) {
-  const unsigned below = act ? (peers & lanemask_lt()) : 0u;
-  const int prev = below ? 31 - __clz(below) : -1;          // previous event of my pixel in the batch
-  const float t_prev_lane = __shfl_sync(kFull, te, prev < 0 ? lane : prev);
-  float s0 = 0.f, tp = t_prev_lane;
-  if (act) {
-    s0 = S[px];                                               // state before the batch
-    if (prev < 0) tp = T[px];
-  }
-  __syncwarp();                                               // all reads before any write
-  const float d = act ? ev_decay<BM>(te - tp, k) : 1.f;
-  float fa = d, fc = d * pc, flo = k.smin, fhi = k.smax;      // f_i
-  int ptr = prev;
-  while (__any_sync(kFull, ptr >= 0)) {
-    const int src = ptr >= 0 ? ptr : lane;
-    const float ga = __shfl_sync(kFull, fa, src), gc = __shfl_sync(kFull, fc, src);
-    const float glo = __shfl_sync(kFull, flo, src), ghi = __shfl_sync(kFull, fhi, src);
-    const int gp = __shfl_sync(kFull, ptr, src);
-    if (ptr >= 0) {                                           // F <- F o G
-      const float nlo = fminf(fmaxf(fmaf(fa, glo, fc), flo), fhi);
-      const float nhi = fminf(fmaxf(fmaf(fa, ghi, fc), flo), fhi);
-      fc = fmaf(fa, gc, fc);
-      fa = fa * ga;
-      flo = nlo;
-      fhi = nhi;
-      ptr = gp;
-    }
-  }
-  const bool single = __popc(peers) == 1;
-  const float v = single ? clampS((s0 + pc) * d, k)                       // direct Alg. 2 body
-                         : fminf(fmaxf(fmaf(fa, s0, fc), flo), fhi);      // prefix_i(s0)
-  const unsigned above = peers & ~lanemask_lt() & ~(1u << lane);
-  if (act && above == 0u) {                                   // last event of its pixel in the batch
-    S[px] = v;
-    T[px] = te;
-  }
-}
-
 // Readout of 2 pixels (reading A4: v = S d(t_j - T), non-mutating; Eq. 13 clamp
 // when the bounds exclude 0; Eq. 14 rounded half away from zero, reading A8).
 // Folded mode (b = 2, integer tau, bounds containing 0): with w = T - (t_j - tau)
@@ -172,23 +115,48 @@ __device__ __forceinline__ uint32_t readout2(float2 s, float2 T, float tj, float
   return __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x0040);  // 2 bytes in the low half
 }
 
-template <int NW, int PPL>
+constexpr int kSlots = 8;   // events of one pixel in one segment applied by a single thread
+constexpr uint32_t kEmpty = 0xffffu;
+constexpr int kNW = 16;                       // warps per CTA
+constexpr int kNT = kNW * 32;                 // threads per CTA
+constexpr int kEPT = 2;                       // events per thread per segment
+constexpr int kSB = kNT * kEPT;               // events per sub-batch
+
+// Shared memory of one CTA, carved at run time (the band size is a run-time
+// multiple of 64 pixels chosen to balance the grid over the SMs).
 struct FastSmem {
-  static constexpr int WPX = 32 * PPL;         // pixels per warp
-  static constexpr int BP = NW * WPX;          // pixels per band
-  static constexpr int SB = NW * 128;          // events per sub-batch (4 per lane in the split)
-  float S[BP];
-  float T[BP];
-  uint2 sub[SB + 2];                          // + the first event of the next sub-batch
-  uint2 lst[SB];
-  uint32_t cnt[NW][NW];                       // [slice warp][owner warp]
-  uint32_t lbeg[NW + 1];
-  uint32_t tiles[1];                          // pre[n_tiles + 1] then mt[n_tiles] (dynamic tail)
+  float* S;                                   // [bp] accumulation (fp32)
+  float* T;                                   // [bp] last time, relative to trel (exact integers)
+  uint32_t* head;                             // [bp] last claimer | generation << 16
+  uint16_t* next;                             // [kSB] previous claimer (claim-order chain)
+  uint2* sub[2];                              // [kSB] gathered sub-batches (double buffer), arrival order
+  uint2* stage;                               // [kNW][64] per-warp scratch: chain heads / dense compaction
+  uint16_t* dq;                               // [kSB / 4] dense pixels of the segment
+  uint32_t* nd;
+  uint32_t* pre;                              // [n_tiles + 1]
+  uint32_t* mt;                               // [n_tiles]
 };
 
-template <int NW, int PPL>
-size_t fast_smem_bytes(int n_tiles) {
-  return sizeof(FastSmem<NW, PPL>) + (size_t)(2 * n_tiles + 1) * sizeof(uint32_t);
+__host__ __device__ inline size_t fast_smem_bytes(int bp, int n_tiles) {
+  const size_t b = (size_t)bp;
+  return b * 12 + kSB * 2 + 2 * kSB * 8 + kNW * 64 * 8 + (kSB / 4) * 2 + 16 + (size_t)(2 * n_tiles + 1) * 4 + 64;
+}
+
+__device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_tiles) {
+  FastSmem m;
+  unsigned char* q = base;
+  m.sub[0] = reinterpret_cast<uint2*>(q); q += kSB * 8;
+  m.sub[1] = reinterpret_cast<uint2*>(q); q += kSB * 8;
+  m.stage = reinterpret_cast<uint2*>(q); q += kNW * 64 * 8;
+  m.S = reinterpret_cast<float*>(q); q += (size_t)bp * 4;
+  m.T = reinterpret_cast<float*>(q); q += (size_t)bp * 4;
+  m.head = reinterpret_cast<uint32_t*>(q); q += (size_t)bp * 4;
+  m.pre = reinterpret_cast<uint32_t*>(q); q += (size_t)(n_tiles + 1) * 4;
+  m.mt = reinterpret_cast<uint32_t*>(q); q += (size_t)n_tiles * 4;
+  m.nd = reinterpret_cast<uint32_t*>(q); q += 16;
+  m.next = reinterpret_cast<uint16_t*>(q); q += kSB * 2;
+  m.dq = reinterpret_cast<uint16_t*>(q);
+  return m;
 }
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
@@ -197,84 +165,277 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int NW, int PPL, int BM>
-__device__ __forceinline__ void fast_readout(const IntArgs& a, FastSmem<NW, PPL>& sm, int j, int64_t trel,
-                                             int64_t px0, int npx, int warp, int lane, const FastConst& c) {
-  const int base = warp * FastSmem<NW, PPL>::WPX + lane * PPL;
-  if (base >= npx) return;
+// Frame j for the band: 4 pixels per thread-iteration (quads), Eq. 4 + Eq. 13 +
+// Eq. 14 with packed f32x2 arithmetic, one 4-byte streaming store per quad.
+template <int BM>
+__device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm, int j, int64_t trel,
+                                             int64_t px0, int npx, const FastConst& c) {
   const int32_t tji = (int32_t)(a.tf[j] - trel);
   const float tj = (float)tji;
   const float aj = (float)(tji - (int32_t)c.tau_h);          // t_j - tau (folded mode: tau integer)
-  const float4 s0 = *reinterpret_cast<const float4*>(&sm.S[base]);
-  const float4 t0 = *reinterpret_cast<const float4*>(&sm.T[base]);
-  const uint32_t b01 = readout2<BM>(make_float2(s0.x, s0.y), make_float2(t0.x, t0.y), tj, aj, c);
-  const uint32_t b23 = readout2<BM>(make_float2(s0.z, s0.w), make_float2(t0.z, t0.w), tj, aj, c);
-  const uint32_t lo = __byte_perm(b01, b23, 0x5410);
-  uint8_t* dst = a.out + (int64_t)j * a.P + px0 + base;
-  if (PPL == 8) {
-    const float4 s1 = *reinterpret_cast<const float4*>(&sm.S[base + 4]);
-    const float4 t1 = *reinterpret_cast<const float4*>(&sm.T[base + 4]);
-    const uint32_t b45 = readout2<BM>(make_float2(s1.x, s1.y), make_float2(t1.x, t1.y), tj, aj, c);
-    const uint32_t b67 = readout2<BM>(make_float2(s1.z, s1.w), make_float2(t1.z, t1.w), tj, aj, c);
-    const uint32_t hi = __byte_perm(b45, b67, 0x5410);
-    if (a.vec8 && base + 8 <= npx) {
-      st_stream8(dst, lo, hi);
-      return;
-    }
-    const int nq = min(8, npx - base);
-    for (int q = 0; q < nq; ++q) dst[q] = (uint8_t)((q < 4 ? lo >> (8 * q) : hi >> (8 * (q - 4))) & 0xffu);
-  } else {
+  uint8_t* frame = a.out + (int64_t)j * a.P + px0;
+  const int nq = (npx + 3) >> 2;
+  for (int q = threadIdx.x; q < nq; q += kNT) {
+    const int base = q * 4;
+    const float4 s0 = *reinterpret_cast<const float4*>(&sm.S[base]);
+    const float4 t0 = *reinterpret_cast<const float4*>(&sm.T[base]);
+    const uint32_t b01 = readout2<BM>(make_float2(s0.x, s0.y), make_float2(t0.x, t0.y), tj, aj, c);
+    const uint32_t b23 = readout2<BM>(make_float2(s0.z, s0.w), make_float2(t0.z, t0.w), tj, aj, c);
+    const uint32_t v = __byte_perm(b01, b23, 0x5410);
     if (a.vec8 && base + 4 <= npx) {
-      st_stream4(dst, lo);
-      return;
+      st_stream4(frame + base, v);
+    } else {
+      const int n = min(4, npx - base);
+      for (int u = 0; u < n; ++u) frame[base + u] = (uint8_t)((v >> (8 * u)) & 0xffu);
     }
-    const int nq = min(4, npx - base);
-    for (int q = 0; q < nq; ++q) dst[q] = (uint8_t)((lo >> (8 * q)) & 0xffu);
   }
 }
 
-template <int NW, int PPL, int BM>
-__global__ void __launch_bounds__(NW * 32, (NW * 32 >= 512) ? 3 : 1536 / (NW * 32)) esi_integrate_kernel(IntArgs a) {
-  using Sm = FastSmem<NW, PPL>;
-  constexpr int WSH = PPL == 8 ? 8 : 7;        // log2(pixels per warp)
-  constexpr int BP = Sm::BP;
-  constexpr int SB = Sm::SB;
-  constexpr int NT = NW * 32;
-  constexpr int ROUNDS = SB / NW / 32;        // = 4: events per lane in the split
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
-  __shared__ uint32_t s_wsum[32];
+// Alg. 2 loop body for one event of pixel px, sequentially.
+template <int BM>
+__device__ __forceinline__ void apply_event(float* S, float* T, int px, uint2 ev, uint32_t trel,
+                                            const FastConst& k) {
+  const float te = (float)(int32_t)(ev.x - trel);
+  const float pc = ((int32_t)ev.y < 0) ? -k.C : k.C;
+  float s = S[px] + pc;                                   // S <- S + p C
+  s *= ev_decay<BM>(te - T[px], k);                       // S <- S max{(1 - k dt)^b, 0}
+  S[px] = clampS(s, k);                                   // S <- min(max(S, S_min), S_max)
+  T[px] = te;                                             // T <- t
+}
 
+// Dense pixel (> kSlots events in the segment): one warp composes the events'
+// clamped affine maps s -> clamp(a s + c, lo, hi), a >= 0:
+// event i is f_i = (d_i, d_i p_i C, S_min, S_max) and
+//   F o G = (aF aG, aF cG + cF, clamp(aF loG + cF, loF, hiF), clamp(aF hiG + cF, loF, hiF)).
+// The segment is scanned 32 events at a time; the pixel's events of each group
+// are compacted to the low lanes (arrival order), their maps are combined by a
+// warp-shuffle inclusive scan, and the last prefix is applied to the state.
+template <int BM>
+__device__ __forceinline__ void dense_pixel_apply(float* S, float* T, const uint2* sub, uint2* stage, int e0,
+                                                  int e1, int q, uint32_t trel, int lane, const FastConst& k) {
+  float s = S[q], tprev = T[q];
+  for (int base = e0; base < e1; base += 32) {
+    const int i = base + lane;
+    const uint2 ev = i < e1 ? sub[i] : make_uint2(0u, 0xffffffffu);
+    const bool mine = i < e1 && (int)(ev.y & 0x7fffffffu) == q;
+    const unsigned m = __ballot_sync(kFull, mine);
+    if (!m) continue;
+    const int nk = __popc(m);
+    if (mine) stage[__popc(m & lanemask_lt())] = ev;     // compact, arrival order kept
+    __syncwarp();
+    const uint2 cev = stage[lane];
+    __syncwarp();
+    const float te = (float)(int32_t)(cev.x - trel);
+    float tp = __shfl_up_sync(kFull, te, 1);
+    if (lane == 0) tp = tprev;
+    const bool act = lane < nk;
+    const float d = act ? ev_decay<BM>(te - tp, k) : 1.f;
+    const float pc = ((int32_t)cev.y < 0) ? -k.C : k.C;
+    float fa = d, fc = act ? d * pc : 0.f, flo = k.smin, fhi = k.smax;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float ga = __shfl_up_sync(kFull, fa, off), gc = __shfl_up_sync(kFull, fc, off);
+      const float glo = __shfl_up_sync(kFull, flo, off), ghi = __shfl_up_sync(kFull, fhi, off);
+      if (lane >= off) {                                  // F <- F o G (G = earlier events)
+        const float nlo = fminf(fmaxf(fmaf(fa, glo, fc), flo), fhi);
+        const float nhi = fminf(fmaxf(fmaf(fa, ghi, fc), flo), fhi);
+        fc = fmaf(fa, gc, fc);
+        fa = fa * ga;
+        flo = nlo;
+        fhi = nhi;
+      }
+    }
+    const float La = __shfl_sync(kFull, fa, nk - 1), Lc = __shfl_sync(kFull, fc, nk - 1);
+    const float Llo = __shfl_sync(kFull, flo, nk - 1), Lhi = __shfl_sync(kFull, fhi, nk - 1);
+    s = fminf(fmaxf(fmaf(La, s, Lc), Llo), Lhi);
+    tprev = __shfl_sync(kFull, te, nk - 1);
+  }
+  if (lane == 0) {
+    S[q] = s;
+    T[q] = tprev;
+  }
+}
+
+// Per-event processing of one segment (the events of one frame window inside
+// one sub-batch), block-wide.  Each event claims its pixel with an atomic
+// exchange on head[px] (tagged with the segment's generation, so the table
+// never needs clearing), which links the pixel's events into a chain in claim
+// order.  The last claimer owns the pixel for the segment: a pixel hit once is
+// updated directly (sparse path); chains of 2..kSlots events are collected per
+// warp and applied one chain per lane after a sorting network restores arrival
+// order; more go to a warp (dense path).  The first two paths are bit-identical
+// to a sequential fp32 evaluation.  Two barriers: claims complete before
+// ownership is read; updates complete before anyone reads the state (readout)
+// or re-claims.
+template <int BM>
+__device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* sub, int e0, int e1, uint32_t trel,
+                                                uint32_t gen, int warp, int lane, const FastConst& k) {
+  const int tid = threadIdx.x;
+  const uint32_t tag = gen << 16;
+  for (int i = e0 + tid; i < e1; i += kNT) {              // claim
+    const int px = (int)(sub[i].y & 0x7fffffffu);
+    const uint32_t old = atomicExch(&sm.head[px], tag | (uint32_t)(i - e0));
+    sm.next[i - e0] = (old & 0xffff0000u) == tag ? (uint16_t)old : (uint16_t)kEmpty;
+  }
+  __syncthreads();
+  uint32_t* wl = reinterpret_cast<uint32_t*>(sm.stage + warp * 64);   // <= kEPT * 32 chain heads
+  int nch = 0;
+  for (int ib = e0; ib < e1; ib += kNT) {                 // apply: singles now, chains deferred
+    const int i = ib + tid;
+    bool chain = false;
+    uint32_t me = 0;
+    if (i < e1) {
+      const uint2 ev = sub[i];
+      const int px = (int)(ev.y & 0x7fffffffu);
+      me = (uint32_t)(i - e0);
+      if (sm.head[px] == (tag | me)) {
+        if (sm.next[me] == kEmpty) apply_event<BM>(sm.S, sm.T, px, ev, trel, k);
+        else chain = true;
+      }
+    }
+    const unsigned bc = __ballot_sync(kFull, chain);
+    if (chain) wl[nch + __popc(bc & lanemask_lt())] = me;
+    nch += __popc(bc);
+  }
+  __syncwarp();
+  for (int cb = 0; cb < nch; cb += 32) {                  // chains: one per lane
+    if (cb + lane >= nch) break;
+    const uint32_t me = wl[cb + lane];
+    const int px = (int)(sub[e0 + me].y & 0x7fffffffu);
+    uint32_t id[kSlots];
+    id[0] = me;
+    int c = 1;
+#pragma unroll
+    for (int q = 1; q < kSlots; ++q) {
+      const uint32_t n = (c == q) ? sm.next[id[q - 1]] : kEmpty;
+      id[q] = n;
+      c += (n != kEmpty) ? 1 : 0;
+    }
+    if (c == kSlots && sm.next[id[kSlots - 1]] != kEmpty) {   // > kSlots events: dense path
+      sm.dq[atomicAdd(sm.nd, 1u)] = (uint16_t)px;
+      continue;
+    }
+    // claim order -> arrival order (kEmpty = 0xffff sorts after every index)
+#define ESI_CSWAP(x, y) { const uint32_t lo_ = min(id[x], id[y]), hi_ = max(id[x], id[y]); id[x] = lo_; id[y] = hi_; }
+    ESI_CSWAP(0, 1) ESI_CSWAP(2, 3) ESI_CSWAP(4, 5) ESI_CSWAP(6, 7)
+    ESI_CSWAP(0, 2) ESI_CSWAP(1, 3) ESI_CSWAP(4, 6) ESI_CSWAP(5, 7)
+    ESI_CSWAP(1, 2) ESI_CSWAP(5, 6) ESI_CSWAP(0, 4) ESI_CSWAP(3, 7)
+    ESI_CSWAP(1, 5) ESI_CSWAP(2, 6)
+    ESI_CSWAP(1, 4) ESI_CSWAP(3, 6)
+    ESI_CSWAP(2, 4) ESI_CSWAP(3, 5)
+    ESI_CSWAP(3, 4)
+#undef ESI_CSWAP
+    float s = sm.S[px], t = sm.T[px];
+    for (int q = 0; q < c; ++q) {
+      uint32_t iq = id[0];
+#pragma unroll
+      for (int u = 1; u < kSlots; ++u) iq = (q == u) ? id[u] : iq;     // register select
+      const uint2 e = sub[e0 + iq];
+      const float te = (float)(int32_t)(e.x - trel);
+      const float pc = ((int32_t)e.y < 0) ? -k.C : k.C;
+      s = clampS((s + pc) * ev_decay<BM>(te - t, k), k);     // Alg. 2 body
+      t = te;
+    }
+    sm.S[px] = s;
+    sm.T[px] = t;
+  }
+  __syncthreads();
+  const uint32_t nd = *sm.nd;
+  if (nd > 0) {
+    for (uint32_t d = warp; d < nd; d += kNW)
+      dense_pixel_apply<BM>(sm.S, sm.T, sub, sm.stage + warp * 64, e0, e1, sm.dq[d], trel, lane, k);
+    __syncthreads();
+    if (tid == 0) *sm.nd = 0;
+  }
+}
+
+// number of sub-batch events in [0, n) with relative time <= tj (times sorted, n <= 1024):
+// warp-wide 2-level 32-ary search, identical in every warp (no barrier needed)
+__device__ __forceinline__ int upper_bound_rel(const uint2* sub, int n, uint32_t trel, int32_t tj, int lane) {
+  static_assert(kSB <= 1024, "2-level search");
+  int lo = 0;
+#pragma unroll
+  for (int stride = 32; stride >= 1; stride >>= 5) {
+    const int p = lo + lane * stride;
+    const bool le = p < n && (int32_t)(sub[p].x - trel) <= tj;
+    const unsigned b = __ballot_sync(kFull, le);
+    if (b == 0u) return lo;                               // sub[lo] > tj (lo is always a candidate)
+    lo += (31 - __clz(b)) * stride;
+  }
+  return lo + 1;
+}
+
+// Gather band events [sb0, min(sb0 + kSB, n_b)) into dst with cp.async: 8 (tile,
+// band) segments per warp step, 4 lanes per segment, tiles in order = arrival order.
+__device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const uint32_t* pre, const uint32_t* mt,
+                                           int n_tiles, int n_b, int sb0, uint2* dst, int warp, int lane) {
+  const uint32_t q_end = (uint32_t)min(sb0 + kSB, n_b);
+  int t_lo;                                     // last tile with pre[t] <= sb0 (32-ary search)
+  {
+    const int c = lane * 32;
+    const unsigned b1 = __ballot_sync(kFull, c < n_tiles && pre[c] <= (uint32_t)sb0);
+    const int blk = 31 - __clz(b1 | 1u);
+    const int t = blk * 32 + lane;
+    const unsigned b2 = __ballot_sync(kFull, t < n_tiles && pre[t] <= (uint32_t)sb0);
+    t_lo = blk * 32 + (31 - __clz(b2 | 1u));
+  }
+  for (int tb = t_lo + warp * 8; tb < n_tiles; tb += kNW * 8) {
+    if (pre[tb] >= q_end) break;                // segments are in order: the rest is later
+    const int t = tb + (lane >> 2);
+    uint32_t i0 = 0, i1 = 0, p0 = 0;
+    const uint2* src = rec;
+    if (t < n_tiles) {
+      p0 = pre[t];
+      const uint32_t m = mt[t];
+      if (p0 < q_end) {
+        i0 = p0 < (uint32_t)sb0 ? (uint32_t)sb0 - p0 : 0u;
+        i1 = min(m >> 16, q_end - p0);
+      }
+      src += (size_t)t * kTile + (m & 0xffffu);
+    }
+    const int dofs = (int)p0 - sb0;             // >= -i0
+    for (uint32_t i = i0 + (lane & 3); i < i1; i += 4) cp_async8(&dst[dofs + (int)i], src + i);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int BM>
+__global__ void __launch_bounds__(kNT, 3) esi_integrate_kernel(IntArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_wsum[32];
   const int band = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t px0 = (int64_t)band * BP;
-  const int npx = (int)min((int64_t)BP, a.P - px0);
+  const int bp = a.band_px;
+  const int64_t px0 = (int64_t)band * bp;
+  const int npx = (int)min((int64_t)bp, a.P - px0);
+  const int n_tiles = a.n_tiles;
+  const FastSmem sm = carve(smem_raw, bp, n_tiles);
 
   const ChunkInfo ci = *a.info;
   const int f_lo = ci.f_lo, f_hi = ci.f_hi;
   const bool active = ci.active != 0;
   if (!active && f_lo >= f_hi) return;
   const int64_t trel = ci.trel;
+  const uint32_t trel32 = (uint32_t)trel;
   const float t_clamp = -(float)(a.dp.dt_cut + 1);
-  const float tcap = (float)min(a.t_cap - trel, (int64_t)(1 << 25));
-  const int n_tiles = a.n_tiles;
-  uint32_t* pre = sm.tiles;                   // [n_tiles + 1]
-  uint32_t* mt = sm.tiles + n_tiles + 1;      // [n_tiles]
+  const int32_t tcap = (int32_t)min(a.t_cap - trel, (int64_t)(1 << 25));
   const FastConst kc = make_const(a);
 
-  for (int i = threadIdx.x; i < BP; i += NT) {
+  for (int i = threadIdx.x; i < bp; i += kNT) {
     const bool in = i < npx;
     sm.S[i] = in ? a.S[px0 + i] : 0.f;
     sm.T[i] = in ? (float)max(a.T[px0 + i] - trel, (int64_t)t_clamp) : t_clamp;
+    sm.head[i] = 0u;                          // generation 0: never a live claim
   }
+  if (threadIdx.x == 0) *sm.nd = 0;
   int n_b = 0;
   if (active) {
-    for (int t = threadIdx.x; t < n_tiles; t += NT) mt[t] = a.meta[(int64_t)band * n_tiles + t];
+    for (int t = threadIdx.x; t < n_tiles; t += kNT) sm.mt[t] = a.meta[(int64_t)band * n_tiles + t];
     __syncthreads();
-    const int per = (n_tiles + NT - 1) / NT;
+    const int per = (n_tiles + kNT - 1) / kNT;
     const int t0 = threadIdx.x * per;
     uint32_t local = 0;
-    for (int t = t0; t < min(n_tiles, t0 + per); ++t) local += mt[t] >> 16;
+    for (int t = t0; t < min(n_tiles, t0 + per); ++t) local += sm.mt[t] >> 16;
     uint32_t x = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -285,169 +446,62 @@ __global__ void __launch_bounds__(NW * 32, (NW * 32 >= 512) ? 3 : 1536 / (NW * 3
     __syncthreads();
     uint32_t run = x - local, tot = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
+    for (int w = 0; w < kNW; ++w) {
       const uint32_t v = s_wsum[w];
       if (w < warp) run += v;
       tot += v;
     }
     for (int t = t0; t < min(n_tiles, t0 + per); ++t) {
-      pre[t] = run;
-      run += mt[t] >> 16;
+      sm.pre[t] = run;
+      run += sm.mt[t] >> 16;
     }
-    if (threadIdx.x == 0) pre[n_tiles] = tot;
+    if (threadIdx.x == 0) sm.pre[n_tiles] = tot;
     n_b = (int)tot;
   }
   __syncthreads();
 
   int j = f_lo;
+  int32_t tj = (j < f_hi) ? (int32_t)(a.tf[j] - trel) : tcap;
   bool done = false;
-  for (int sb0 = 0; sb0 < n_b; sb0 += SB) {
-    const int n_sb = min(SB, n_b - sb0);
-    const bool has_next = sb0 + n_sb < n_b;
-    const uint32_t q_end = (uint32_t)(sb0 + n_sb);
-    // ---- 1. gather the sub-batch + the next sub-batch's first event (cp.async,
-    //         one warp per (tile, band) segment, tiles in order = arrival order)
-    // last tile with pre[t] <= sb0: 32-ary search by each warp (n_tiles <= 1024)
-    int t_lo;
-    {
-      const int c = lane * 32;
-      const unsigned b1 = __ballot_sync(kFull, c < n_tiles && pre[c] <= (uint32_t)sb0);
-      const int blk = 31 - __clz(b1 | 1u);
-      const int t = blk * 32 + lane;
-      const unsigned b2 = __ballot_sync(kFull, t < n_tiles && pre[t] <= (uint32_t)sb0);
-      t_lo = blk * 32 + (31 - __clz(b2 | 1u));
-    }
-    // 8 segments per warp step, 4 lanes per segment (one 32-B sector per copy step)
-    for (int tb = t_lo + warp * 8; tb < n_tiles; tb += NW * 8) {
-      if (pre[tb] > q_end) break;               // segments are in order: the rest is later
-      const int t = tb + (lane >> 2);
-      uint32_t i0 = 0, i1 = 0, p0 = 0;
-      const uint2* src = a.rec;
-      if (t < n_tiles) {
-        p0 = pre[t];
-        const uint32_t m = mt[t];
-        if (p0 <= q_end) {
-          i0 = p0 < (uint32_t)sb0 ? (uint32_t)sb0 - p0 : 0u;
-          i1 = min(m >> 16, q_end + 1 - p0);
-        }
-        src += (size_t)t * kTile + (m & 0xffffu);
-      }
-      const int dofs = (int)p0 - sb0;           // >= -i0
-      for (uint32_t i = i0 + (lane & 3); i < i1; i += 4) cp_async8(&sm.sub[dofs + (int)i], src + i);
-    }
-    if (lane < NW) sm.cnt[warp][lane] = 0;
+  uint32_t gen = 0;
+  // ---- 1. gather sub-batch k into sub[k & 1]; sub-batch k+1 is in flight while k is integrated
+  if (n_b > 0) gather_sub(a.rec, sm.pre, sm.mt, n_tiles, n_b, 0, sm.sub[0], warp, lane);
+  for (int sb0 = 0, kb = 0; sb0 < n_b && !done; sb0 += kSB, ++kb) {
+    const int n_sb = min(kSB, n_b - sb0);
+    const uint2* sub = (kb & 1) ? sm.sub[1] : sm.sub[0];   // no dynamic index into sm (keeps it in registers)
     cp_async_wait_all();
     __syncthreads();
-    const float tnext = has_next ? (float)(int32_t)(sm.sub[n_sb].x - (uint32_t)trel) : 3.0e38f;
-    // ---- 2a. rank each event of slice `warp` among the slice's events for the same owner
-    uint2 rec[ROUNDS];
-    uint32_t pos[ROUNDS];
-#pragma unroll
-    for (int r = 0; r < ROUNDS; ++r) {
-      const int i = warp * (ROUNDS * 32) + r * 32 + lane;
-      const bool act = i < n_sb;
-      rec[r] = act ? sm.sub[i] : make_uint2(0u, 0u);
-      rec[r].x = __float_as_uint((float)(int32_t)(rec[r].x - (uint32_t)trel));   // relative time, exact
-      const int own = act ? (int)((rec[r].y & (uint32_t)(BP - 1)) >> WSH) : NW + lane;
-      const unsigned peers = __match_any_sync(kFull, own);
-      const uint32_t rank = __popc(peers & lanemask_lt());
-      uint32_t base = 0;
-      if (act) base = sm.cnt[warp][own];
-      __syncwarp();
-      if (act && rank == 0) sm.cnt[warp][own] = base + __popc(peers);
-      __syncwarp();
-      pos[r] = act ? ((base + rank) | ((uint32_t)own << 16)) : 0xffffffffu;
-    }
-    __syncthreads();
-    // ---- 2b. exclusive scan of the [slice][owner] counts (owner-major)
-    if (threadIdx.x < NW) {
-      const int own = threadIdx.x;
-      uint32_t run = 0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t c = sm.cnt[w][own];
-        sm.cnt[w][own] = run;
-        run += c;
-      }
-      sm.lbeg[own + 1] = run;                  // owner total, prefixed below
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t run = 0;
-      sm.lbeg[0] = 0;
-      for (int w = 0; w < NW; ++w) {
-        run += sm.lbeg[w + 1];
-        sm.lbeg[w + 1] = run;
-      }
-    }
-    __syncthreads();
-    // ---- 2c. stable scatter to the owners' lists
-#pragma unroll
-    for (int r = 0; r < ROUNDS; ++r) {
-      if (pos[r] != 0xffffffffu) {
-        const int own = (int)(pos[r] >> 16);
-        sm.lst[sm.lbeg[own] + sm.cnt[warp][own] + (pos[r] & 0xffffu)] = rec[r];
-      }
-    }
-    __syncthreads();
-
-    // ---- 3. walk: apply events, reading frames out at their boundaries
-    const int l_end = (int)sm.lbeg[warp + 1];
-    int i = (int)sm.lbeg[warp];
-    float tj = (j < f_hi) ? (float)(int32_t)(a.tf[j] - trel) : tcap;
-    while (!done && i < l_end) {
-      const int m = min(32, l_end - i);
-      float te = 0.f;
-      uint32_t pr = 0;
-      if (lane < m) {
-        const uint2 r = sm.lst[i + lane];
-        te = __uint_as_float(r.x);
-        pr = r.y;
-      }
-      const bool valid = lane < m && te <= tj;
-      const int nv = __popc(__ballot_sync(kFull, valid));
-      if (nv > 0) {
-        const bool act = lane < nv;
-        const int px = (int)(pr & (uint32_t)(BP - 1));
-        const unsigned peers = __match_any_sync(kFull, act ? px : BP + lane);
-        const float pc = ((int32_t)pr < 0) ? -kc.C : kc.C;
-        if (!__any_sync(kFull, act && __popc(peers) > 1)) {
-          // sparse batch: Alg. 2 body applied directly
-          if (act) {
-            float s = sm.S[px] + pc;                                     // S <- S + p C
-            s *= ev_decay<BM>(te - sm.T[px], kc);                        // S <- S d(t - T)
-            sm.S[px] = clampS(s, kc);                                    // clamp (Eq. 13)
-            sm.T[px] = te;                                               // T <- t
-          }
-        } else {
-          dense_batch_apply<BM>(sm.S, sm.T, act, px, peers, te, pc, lane, kc);
+    if (sb0 + kSB < n_b) gather_sub(a.rec, sm.pre, sm.mt, n_tiles, n_b, sb0 + kSB, (kb & 1) ? sm.sub[0] : sm.sub[1], warp, lane);
+    // ---- 2. segments = frame windows inside the sub-batch; readout at each window end
+    int e0 = 0;
+    while (true) {
+      const int e1 = e0 + upper_bound_rel(sub + e0, n_sb - e0, trel32, tj, lane);   // same in every warp
+      if (e1 > e0) {
+        if (++gen == 0xffffu) {                 // generation tags exhausted: clear the claim table
+          __syncthreads();
+          for (int i = threadIdx.x; i < bp; i += kNT) sm.head[i] = 0u;
+          __syncthreads();
+          gen = 1;
         }
-        __syncwarp();
+        process_segment<BM>(sm, sub, e0, e1, trel32, gen, warp, lane, kc);
       }
-      i += nv;
-      if (nv < m) {
-        if (j < f_hi) {
-          fast_readout<NW, PPL, BM>(a, sm, j, trel, px0, npx, warp, lane, kc);
-          ++j;
-          tj = (j < f_hi) ? (float)(int32_t)(a.tf[j] - trel) : tcap;
-        } else {
-          done = true;  // the rest is later than the last frame: stays pending
-        }
-      }
-    }
-    // ---- 4. frames whose events are all in this or earlier sub-batches
-    while (j < f_hi && (float)(int32_t)(a.tf[j] - trel) < tnext) {
-      fast_readout<NW, PPL, BM>(a, sm, j, trel, px0, npx, warp, lane, kc);
+      if (e1 == n_sb) break;                    // the window may continue in the next sub-batch
+      if (j >= f_hi) { done = true; break; }    // later events stay pending
+      fast_readout<BM>(a, sm, j, trel, px0, npx, kc);
       ++j;
+      tj = (j < f_hi) ? (int32_t)(a.tf[j] - trel) : tcap;
+      e0 = e1;
     }
   }
+  cp_async_wait_all();
+  // ---- 3. frames after the chunk's last event
   while (j < f_hi) {
-    fast_readout<NW, PPL, BM>(a, sm, j, trel, px0, npx, warp, lane, kc);
+    fast_readout<BM>(a, sm, j, trel, px0, npx, kc);
     ++j;
   }
   if (n_b > 0) {
     __syncthreads();
-    for (int i = threadIdx.x; i < npx; i += NT) {
+    for (int i = threadIdx.x; i < npx; i += kNT) {
       a.S[px0 + i] = sm.S[i];
       const float tr = sm.T[i];
       if (tr != t_clamp) a.T[px0 + i] = trel + (int64_t)tr;
@@ -455,38 +509,27 @@ __global__ void __launch_bounds__(NW * 32, (NW * 32 >= 512) ? 3 : 1536 / (NW * 3
   }
 }
 
-template <int NW, int PPL, int BM>
-cudaError_t launch_fast_t(const IntArgs& a, cudaStream_t s) {
-  const size_t smem = fast_smem_bytes<NW, PPL>(a.n_tiles);
+template <int BM>
+cudaError_t launch_fast_b(const IntArgs& a, cudaStream_t s) {
+  const size_t smem = fast_smem_bytes(a.band_px, a.n_tiles);
   static size_t configured = 0;
   if (smem > configured) {
-    const size_t mx = fast_smem_bytes<NW, PPL>(kMaxTilesPerChunk);
-    cudaError_t e = cudaFuncSetAttribute(esi_integrate_kernel<NW, PPL, BM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    const size_t mx = fast_smem_bytes(kMaxBandPx, kMaxTilesPerChunk);
+    cudaError_t e = cudaFuncSetAttribute(esi_integrate_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)mx);
     if (e != cudaSuccess) return e;
     configured = mx;
   }
-  esi_integrate_kernel<NW, PPL, BM><<<a.nb, NW * 32, smem, s>>>(a);
+  esi_integrate_kernel<BM><<<a.nb, kNT, smem, s>>>(a);
   return cudaGetLastError();
-}
-
-// warps of 128 pixels (4 per lane) for bands up to 2048 pixels, 256 (8 per lane) above
-template <int BM>
-cudaError_t launch_fast_nw(const IntArgs& a, cudaStream_t s) {
-  switch (a.band_px) {
-    case 256: return launch_fast_t<2, 4, BM>(a, s);
-    case 512: return launch_fast_t<4, 4, BM>(a, s);
-    case 1024: return launch_fast_t<8, 4, BM>(a, s);
-    case 2048: return launch_fast_t<16, 4, BM>(a, s);
-    case 4096: return launch_fast_t<16, 8, BM>(a, s);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 }  // namespace
 
+size_t integrate_fast_smem_bytes(int band_px, int n_tiles) { return fast_smem_bytes(band_px, n_tiles); }
+
 cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s) {
-  return a.dp.bmode == 2 ? launch_fast_nw<2>(a, s) : launch_fast_nw<0>(a, s);
+  return a.dp.bmode == 2 ? launch_fast_b<2>(a, s) : launch_fast_b<0>(a, s);
 }
 
 }  // namespace esi

@@ -18,8 +18,9 @@
 
 namespace esi {
 
-constexpr int kTile = 8192;          // events per partition CTA
+constexpr int kTile = 8192;          // events per partition tile
 constexpr int kPartThreads = 512;    // 16 warps x 16 events per thread
+constexpr int kPartWarps = kPartThreads / 32;
 constexpr int kSubBatch = 1024;      // band events staged in smem per sub-batch
 constexpr int kMaxTilesPerChunk = 1024;
 constexpr int kWarpPx = 256;         // pixels owned by one warp (8 per lane)
@@ -68,9 +69,11 @@ struct PartArgs {
   const int64_t* prev_t;     // t of the event preceding ev[0] (device address)
   int64_t t_origin;
   int64_t last_frame_t;      // events must be > this (INT64_MIN if no frame yet)
+  int64_t t_min;             // max(t_origin, last_frame_t + 1): smallest admissible t
   int64_t t_cap;             // last frame time of the render call
   int32_t W, H;
-  int32_t band_shift, nb, nb_bits;
+  int32_t band_px, nb;
+  uint64_t band_magic;       // pid / band_px = (pid * band_magic) >> 40 (exact for pid < 2^23)
   uint2* rec;                // [n_tiles * kTile] tile-local band-sorted records
   uint32_t* meta;            // [nb][n_tiles]: offset | count << 16
   int64_t* tile_t0;          // [n_tiles]
@@ -132,6 +135,7 @@ struct RouteRows {
 
 size_t partition_smem_bytes(int nb);
 size_t integrate_smem_bytes(int band_px);
+size_t integrate_fast_smem_bytes(int band_px, int n_tiles);
 cudaError_t launch_partition(const PartArgs& a, int n_tiles, bool atomic_rank, cudaStream_t s);
 cudaError_t probe_atomic_order(unsigned* d_bad, cudaStream_t s);
 cudaError_t launch_integrate(const IntArgs& a, cudaStream_t s);

@@ -3,7 +3,7 @@
 // One CTA per tile of kTile (8192) consecutive pending events.  Each lane loads
 // one 16-byte esi_event_t per step (a warp reads 512 contiguous bytes), checks
 // it (reading A15: t non-decreasing, >= t_origin, > last frame),
-// and computes its pixel id y*W + x and its band = pid >> band_shift.  The tile
+// and computes its pixel id y*W + x and its band = pid / band_px.  The tile
 // is then stably partitioned by band -- band-major, arrival-order-minor, i.e.
 // exactly std::stable_sort by band -- with
 //   * warp multi-split ranks from ballots over the band bits (no atomics, so
@@ -20,17 +20,20 @@ namespace esi {
 
 size_t partition_smem_bytes(int nb) {
   const int nbp = (nb + 1) & ~1;
-  return (size_t)kTile * sizeof(uint2) + (size_t)16 * nbp * sizeof(uint16_t) +
+  return (size_t)kTile * sizeof(uint2) + (size_t)kPartWarps * nbp * sizeof(uint16_t) +
          (size_t)(nb + 1) * sizeof(uint32_t) + 64 * sizeof(uint32_t);
 }
 
-// Exclusive scan of v[0..n) in place (n <= 2 * kPartThreads); v[n] = total.
+// Exclusive scan of v[0..n) in place (n <= 4 * kPartThreads); v[n] = total.
 __device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int i0 = 2 * tid;
-  const uint32_t a0 = i0 < n ? v[i0] : 0u;
-  const uint32_t a1 = i0 + 1 < n ? v[i0 + 1] : 0u;
-  const uint32_t s = a0 + a1;
+  const int i0 = 4 * tid;
+  uint32_t a[4], s = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    a[q] = i0 + q < n ? v[i0 + q] : 0u;
+    s += a[q];
+  }
   uint32_t x = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -40,7 +43,7 @@ __device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
   if (lane == 31) wsum[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    uint32_t w = lane < kPartThreads / 32 ? wsum[lane] : 0u;
+    uint32_t w = lane < kPartWarps ? wsum[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, w, o);
@@ -49,10 +52,13 @@ __device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
     wsum[32 + lane] = w;  // inclusive warp totals
   }
   __syncthreads();
-  const uint32_t excl = x - s + (warp ? wsum[32 + warp - 1] : 0u);
-  if (i0 < n) v[i0] = excl;
-  if (i0 + 1 < n) v[i0 + 1] = excl + a0;
-  if (tid == 0) v[n] = wsum[32 + kPartThreads / 32 - 1];
+  uint32_t run = x - s + (warp ? wsum[32 + warp - 1] : 0u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (i0 + q < n) v[i0 + q] = run;
+    run += a[q];
+  }
+  if (tid == 0) v[n] = wsum[32 + kPartWarps - 1];
 }
 
 // RANK_ATOMIC: per-warp rank from a shared-memory atomicAdd on the warp's private
@@ -64,8 +70,8 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
   extern __shared__ __align__(16) unsigned char smem[];
   const int nbp = (a.nb + 1) & ~1;
   uint2* sbuf = reinterpret_cast<uint2*>(smem);
-  uint16_t* hist = reinterpret_cast<uint16_t*>(sbuf + kTile);    // [16][nbp]
-  uint32_t* boff = reinterpret_cast<uint32_t*>(hist + 16 * nbp);  // [nb + 1]
+  uint16_t* hist = reinterpret_cast<uint16_t*>(sbuf + kTile);    // [kPartWarps][nbp]
+  uint32_t* boff = reinterpret_cast<uint32_t*>(hist + kPartWarps * nbp);  // [nb + 1]
   uint32_t* wsum = boff + a.nb + 1;                               // [64]
   __shared__ int s_wide;
 
@@ -78,14 +84,19 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const esi_event_t* ev = a.ev + e0;
   const int4* evv = reinterpret_cast<const int4*>(ev);
-  const uint32_t band_mask = (1u << a.band_shift) - 1u;
 
-  for (int i = threadIdx.x; i < 16 * nbp; i += kPartThreads) hist[i] = 0;
+  for (int i = threadIdx.x; i < kPartWarps * nbp; i += kPartThreads) hist[i] = 0;
   __syncthreads();
 
   uint16_t* myhist = hist + warp * nbp;
   uint2 rec[16];
   uint32_t rk[16];
+  // t of the event preceding this warp's first event (later rounds take it from lane 31)
+  int64_t t_before = 0;
+  if (lane == 0 && warp * 512 < ne) {
+    const int i0 = warp * 512;
+    t_before = (i0 > 0) ? ev[i0 - 1].t_us : (tile > 0 ? ev[-1].t_us : *a.prev_t);
+  }
 
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
@@ -105,20 +116,21 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
       uint32_t y = (uint32_t)raw[u].z >> 16;
       int p = (int)(int8_t)(raw[u].w & 0xff);
       int64_t tp = __shfl_up_sync(kFull, t, 1);
-      if (lane == 0 && act) tp = (i > 0) ? ev[i - 1].t_us : (tile > 0 ? ev[-1].t_us : *a.prev_t);
-      if (act) {
-        int code = 0;
+      if (lane == 0) tp = t_before;
+      t_before = __shfl_sync(kFull, t, 31);
+      // validation (reading A15), one combined test on the common path
+      if (act && (x >= (uint32_t)a.W || y >= (uint32_t)a.H || (unsigned)(p + 1) > 2u || p == 0 ||
+                  t < a.t_min || t < tp)) {
+        int code;
         if (x >= (uint32_t)a.W || y >= (uint32_t)a.H) code = ESI_ERR_OUT_OF_BOUNDS;
         else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
-        else if (t < a.t_origin || t < tp || t <= a.last_frame_t) code = ESI_ERR_NEGATIVE_INTERVAL;
-        if (code) {
-          atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + i) << 8) | (unsigned)code);
-          x = 0; y = 0; p = 1;   // keep the pipeline well-defined; the call reports the error
-        }
+        else code = ESI_ERR_NEGATIVE_INTERVAL;
+        atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + i) << 8) | (unsigned)code);
+        x = 0; y = 0; p = 1;   // keep the pipeline well-defined; the call reports the error
       }
       const uint32_t pid = y * (uint32_t)a.W + x;
-      const uint32_t band = act ? (pid >> a.band_shift) : 0u;
-      rec[r] = make_uint2((uint32_t)t, (pid & band_mask) | (p < 0 ? 0x80000000u : 0u));
+      const uint32_t band = act ? (uint32_t)(((uint64_t)pid * a.band_magic) >> 40) : 0u;
+      rec[r] = make_uint2((uint32_t)t, (pid - band * (uint32_t)a.band_px) | (p < 0 ? 0x80000000u : 0u));
       uint32_t base, rank;
       if (RANK_ATOMIC) {
         uint32_t* hw = reinterpret_cast<uint32_t*>(myhist);
@@ -150,11 +162,11 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
   }
   __syncthreads();
 
-  // per band: exclusive prefix over the 16 warps, band total into boff[band]
+  // per band: exclusive prefix over the warps, band total into boff[band]
   for (int b = threadIdx.x; b < a.nb; b += kPartThreads) {
     uint32_t run = 0;
 #pragma unroll
-    for (int w = 0; w < 16; ++w) {
+    for (int w = 0; w < kPartWarps; ++w) {
       const uint32_t c = hist[w * nbp + b];
       hist[w * nbp + b] = (uint16_t)run;
       run += c;

@@ -49,7 +49,8 @@ struct esi_handle {
   int32_t W = 0, H = 0;
   int64_t P = 0;
   esi_params_t prm{};
-  int band_shift = 8, band_px = 256, nb = 1, nb_bits = 0;
+  int band_px = 256, nb = 1;
+  uint64_t band_magic = 0;
   int64_t chunk_events = 0;
   int max_tiles = 0;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -307,7 +308,7 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   if (params) prm = *params; else esi_default_params(&prm);
   if (width < 1 || height < 1 || width > 65535 || height > 65535) return ESI_ERR_INVALID_ARG;
   const int64_t P = (int64_t)width * height;
-  if (P > (int64_t)kMaxBands * kMaxBandPx) return ESI_ERR_INVALID_ARG;
+  if (P > (int64_t)kMaxBands * kMaxBandPx) return ESI_ERR_INVALID_ARG;   // <= 1024 bands of <= 4096 px
   if (!params_ok(&prm)) return ESI_ERR_INVALID_ARG;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || prm.device < 0 || prm.device >= ndev) {
@@ -322,22 +323,26 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   h->P = P;
   h->prm = prm;
   derive_params(h);
-  // Band size (K1 partition key, K2 CTA): the largest power-of-two multiple of
-  // 256 pixels that still gives >= 2 bands per SM (2 x 148), so that K2's
-  // (tile, band) segments are as long as possible without starving the grid;
-  // never more than kMaxBands bands (K1's shared-memory histograms).
-  h->band_px = kWarpPx;
-  while (h->band_px < kMaxBandPx && (P + 2 * h->band_px - 1) / (2 * h->band_px) >= 296) h->band_px <<= 1;
-  while ((P + h->band_px - 1) / h->band_px > kMaxBands) h->band_px <<= 1;
-  if (const char* bp = getenv("ESI_BAND_PX")) {
-    const int v = atoi(bp);
-    if (v >= kWarpPx && v <= kMaxBandPx && (v & (v - 1)) == 0 && (P + v - 1) / v <= kMaxBands) h->band_px = v;
+  // Band size (K1 partition key, K2 CTA): a multiple of 64 pixels such that
+  // the bands fill the SMs evenly at 3 resident K2 CTAs per SM (c4: 437 bands of
+  // 2112 pixels on 148 SMs), at most kMaxBandPx (shared memory) and at most
+  // kMaxBands bands (K1's shared-memory histograms).
+  {
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, prm.device);
+    const int64_t slots = (int64_t)n_sm * 3;
+    int64_t bp = (P + slots - 1) / slots;
+    bp = ((bp + 63) / 64) * 64;
+    bp = std::max<int64_t>(64, std::min<int64_t>(bp, kMaxBandPx));
+    while ((P + bp - 1) / bp > kMaxBands) bp += 64;
+    if (const char* e = getenv("ESI_BAND_PX")) {
+      const int64_t v = atoll(e);
+      if (v >= 64 && v <= kMaxBandPx && v % 64 == 0 && (P + v - 1) / v <= kMaxBands) bp = v;
+    }
+    h->band_px = (int)bp;
   }
-  h->band_shift = 0;
-  while ((1 << h->band_shift) < h->band_px) ++h->band_shift;
   h->nb = (int)((P + h->band_px - 1) / h->band_px);
-  h->nb_bits = 0;
-  while ((1 << h->nb_bits) < h->nb) ++h->nb_bits;
+  h->band_magic = ((uint64_t)1 << 40) / (uint64_t)h->band_px + 1;   // exact pid / band_px for pid < 2^23
   int64_t ce = prm.chunk_events > 0 ? prm.chunk_events : (int64_t)4 << 20;
   ce = ((ce + kTile - 1) / kTile) * kTile;
   ce = std::min<int64_t>(ce, (int64_t)kMaxTilesPerChunk * kTile);
@@ -363,7 +368,9 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
                 cudaEventCreateWithFlags(&h->ev_k2[b], cudaEventDisableTiming) != cudaSuccess))
       rc = ESI_ERR_CUDA;
   }
-  if (!rc && (cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
+  int prio_lo = 0, prio_hi = 0;   // K1 (aux) at the lowest priority: it fills the SMs around K2
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (!rc && (cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
               cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) != cudaSuccess))
     rc = ESI_ERR_CUDA;
   dalloc((void**)&h->d_err, sizeof(unsigned long long));
@@ -591,12 +598,13 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.prev_t = (c == 0) ? h->d_last_t : &chunks[c - 1].ptr[chunks[c - 1].n - 1].t_us;
       pa.t_origin = h->prm.t_origin_us;
       pa.last_frame_t = h->has_last_frame ? h->last_frame_t : INT64_MIN;
+      pa.t_min = h->has_last_frame ? std::max(h->prm.t_origin_us, h->last_frame_t + 1) : h->prm.t_origin_us;
       pa.t_cap = t_cap;
       pa.W = h->W;
       pa.H = h->H;
-      pa.band_shift = h->band_shift;
+      pa.band_px = h->band_px;
       pa.nb = h->nb;
-      pa.nb_bits = h->nb_bits;
+      pa.band_magic = h->band_magic;
       pa.rec = h->rec[bf];
       pa.meta = h->meta[bf];
       pa.tile_t0 = h->tile_t0[bf];
@@ -792,12 +800,13 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   pa.prev_t = h->d_last_t;
   pa.t_origin = h->prm.t_origin_us;
   pa.last_frame_t = h->has_last_frame ? h->last_frame_t : INT64_MIN;
+  pa.t_min = h->has_last_frame ? std::max(h->prm.t_origin_us, h->last_frame_t + 1) : h->prm.t_origin_us;
   pa.t_cap = INT64_MAX;
   pa.W = h->W;
   pa.H = h->H;
-  pa.band_shift = h->band_shift;
+  pa.band_px = h->band_px;
   pa.nb = h->nb;
-  pa.nb_bits = h->nb_bits;
+  pa.band_magic = h->band_magic;
   pa.rec = h->rec[0];
   pa.meta = h->meta[0];
   pa.tile_t0 = h->tile_t0[0];
