@@ -400,7 +400,7 @@ __device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const 
 }
 
 template <int BM>
-__global__ void __launch_bounds__(kNT, 3) esi_integrate_kernel(IntArgs a) {
+__global__ void __launch_bounds__(kNT, 2) esi_integrate_kernel(IntArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_wsum[32];
   const int band = blockIdx.x;

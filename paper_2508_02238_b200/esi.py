@@ -19,7 +19,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libesi.so")
+LIB_PATH = os.environ.get("ESI_LIB_PATH") or os.path.join(_HERE, "libesi.so")   # override: A/B kernel variants
 
 ESI_OK = 0
 ESI_ERR_INVALID_ARG = 1
