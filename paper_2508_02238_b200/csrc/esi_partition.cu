@@ -61,13 +61,20 @@ __device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
   if (tid == 0) v[n] = wsum[32 + kPartWarps - 1];
 }
 
+// Per-event register state between the ranking and the scatter (32 bits, plus
+// the low 32 bits of t): pixel-in-band (12) | sign of p (1) | warp-local rank
+// within the band (9, < 512 events per warp) | band (10, nb <= 1024).
+__device__ __forceinline__ uint32_t pack_rk(uint32_t pix, bool neg, uint32_t rank, uint32_t band) {
+  return pix | (neg ? 0x1000u : 0u) | (rank << 13) | (band << 22);
+}
+
 // RANK_ATOMIC: per-warp rank from a shared-memory atomicAdd on the warp's private
 // (u16-packed) histogram -- relies on same-address lanes being served in lane
 // order, which esi_probe_atomic_order checks at esi_create; otherwise ranks come
 // from a ballot multi-split over the band bits (order by construction).
-template <bool RANK_ATOMIC>
-__global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// FULL: the tile holds kTile events (no bounds checks on the common path).
+template <bool RANK_ATOMIC, bool FULL>
+__device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char* smem, int tile, int ne) {
   const int nbp = (a.nb + 1) & ~1;
   uint2* sbuf = reinterpret_cast<uint2*>(smem);
   uint16_t* hist = reinterpret_cast<uint16_t*>(sbuf + kTile);    // [kPartWarps][nbp]
@@ -75,89 +82,85 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
   uint32_t* wsum = boff + a.nb + 1;                               // [64]
   __shared__ int s_wide;
 
-  // Chunk entirely after the last frame of this render: nothing to integrate.
-  if (a.ev[0].t_us > a.t_cap) return;
-
-  const int tile = blockIdx.x;
   const int64_t e0 = (int64_t)tile * kTile;
-  const int ne = (int)min((int64_t)kTile, a.n - e0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const esi_event_t* ev = a.ev + e0;
-  const int4* evv = reinterpret_cast<const int4*>(ev);
+  const int4* evw = reinterpret_cast<const int4*>(ev) + warp * 512 + lane;   // this lane's first event
 
   for (int i = threadIdx.x; i < kPartWarps * nbp; i += kPartThreads) hist[i] = 0;
-  __syncthreads();
-
-  uint16_t* myhist = hist + warp * nbp;
-  uint2 rec[16];
-  uint32_t rk[16];
   // t of the event preceding this warp's first event (later rounds take it from lane 31)
   int64_t t_before = 0;
-  if (lane == 0 && warp * 512 < ne) {
+  if (lane == 0 && (FULL || warp * 512 < ne)) {
     const int i0 = warp * 512;
     t_before = (i0 > 0) ? ev[i0 - 1].t_us : (tile > 0 ? ev[-1].t_us : *a.prev_t);
   }
+  __syncthreads();
+
+  uint16_t* myhist = hist + warp * nbp;
+  uint32_t rk[16];   // t is re-read (L2) at the scatter: keeps the ranking loop within 64 registers
+  const uint32_t W = (uint32_t)a.W, H = (uint32_t)a.H, BPX = (uint32_t)a.band_px;
+  const int64_t t_min = a.t_min;
 
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
     int4 raw[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int i = warp * 512 + (g * 4 + u) * 32 + lane;
-      raw[u] = (i < ne) ? ld_stream16(evv + i) : make_int4(0, 0, 0, 0);
+      const int r = g * 4 + u;
+      raw[u] = (FULL || warp * 512 + r * 32 + lane < ne) ? ld_stream16(evw + r * 32) : make_int4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int r = g * 4 + u;
-      const int i = warp * 512 + r * 32 + lane;
-      const bool act = i < ne;
+      const bool act = FULL || warp * 512 + r * 32 + lane < ne;
       const int64_t t = (int64_t)(((uint64_t)(uint32_t)raw[u].y << 32) | (uint32_t)raw[u].x);
       uint32_t x = (uint32_t)raw[u].z & 0xffffu;
       uint32_t y = (uint32_t)raw[u].z >> 16;
-      int p = (int)(int8_t)(raw[u].w & 0xff);
+      const int p = (int)(int8_t)(raw[u].w & 0xff);
       int64_t tp = __shfl_up_sync(kFull, t, 1);
       if (lane == 0) tp = t_before;
       t_before = __shfl_sync(kFull, t, 31);
       // validation (reading A15), one combined test on the common path
-      if (act && (x >= (uint32_t)a.W || y >= (uint32_t)a.H || (unsigned)(p + 1) > 2u || p == 0 ||
-                  t < a.t_min || t < tp)) {
+      const bool bad = (x >= W) | (y >= H) | (p * p != 1) | (t < t_min) | (t < tp);
+      if (act && bad) {
         int code;
-        if (x >= (uint32_t)a.W || y >= (uint32_t)a.H) code = ESI_ERR_OUT_OF_BOUNDS;
+        if (x >= W || y >= H) code = ESI_ERR_OUT_OF_BOUNDS;
         else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
         else code = ESI_ERR_NEGATIVE_INTERVAL;
-        atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + i) << 8) | (unsigned)code);
-        x = 0; y = 0; p = 1;   // keep the pipeline well-defined; the call reports the error
+        atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + warp * 512 + r * 32 + lane) << 8) |
+                             (unsigned)code);
+        x = 0; y = 0;            // keep the pipeline well-defined; the call reports the error
       }
-      const uint32_t pid = y * (uint32_t)a.W + x;
+      const uint32_t pid = y * W + x;
       const uint32_t band = act ? (uint32_t)(((uint64_t)pid * a.band_magic) >> 40) : 0u;
-      rec[r] = make_uint2((uint32_t)t, (pid - band * (uint32_t)a.band_px) | (p < 0 ? 0x80000000u : 0u));
-      uint32_t base, rank;
+      const uint32_t pix = pid - band * BPX;
+      uint32_t rank;
       if (RANK_ATOMIC) {
         uint32_t* hw = reinterpret_cast<uint32_t*>(myhist);
         const uint32_t sh = (band & 1u) << 4;
         const uint32_t old = act ? atomicAdd(hw + (band >> 1), 1u << sh) : 0u;
-        base = (old >> sh) & 0xffffu;
-        rank = 0;
+        rank = (old >> sh) & 0xffffu;
       } else {
         // warp multi-split: lanes whose band equals mine
         unsigned peers = __ballot_sync(kFull, act);
 #pragma unroll
-        for (int bit = 0; bit < 10; ++bit) {   // nb <= 1024: bits above nb_bits are 0 in every lane
+        for (int bit = 0; bit < 10; ++bit) {   // nb <= 1024
           const bool bset = (band >> bit) & 1u;
           const unsigned bb = __ballot_sync(kFull, bset);
           peers &= bset ? bb : ~bb;
         }
         if (!act) peers = 0u;
-        rank = __popc(peers & lanemask_lt());
-        base = 0;
-        if (act && rank == 0) {
+        const uint32_t rl = __popc(peers & lanemask_lt());
+        uint32_t base = 0;
+        if (act && rl == 0) {
           base = myhist[band];
           myhist[band] = (uint16_t)(base + __popc(peers));
         }
         base = __shfl_sync(kFull, base, act ? (__ffs(peers) - 1) : lane);
         __syncwarp();
+        rank = base + rl;
       }
-      rk[r] = (base + rank) | (band << 16);
+      rk[r] = pack_rk(pix, p < 0 && !(act && bad), rank, band);
     }
   }
   __syncthreads();
@@ -181,13 +184,13 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
     const uint32_t cnt = boff[b + 1] - boff[b];
     a.meta[(int64_t)b * gridDim.x + tile] = boff[b] | (cnt << 16);
   }
+  const uint32_t* tlo = reinterpret_cast<const uint32_t*>(ev) + 4 * (warp * 512 + lane);   // low words of t
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const int i = warp * 512 + r * 32 + lane;
-    if (i < ne) {
-      const uint32_t band = rk[r] >> 16;
-      const uint32_t pos = boff[band] + hist[warp * nbp + band] + (rk[r] & 0xffffu);
-      sbuf[pos] = rec[r];
+    if (FULL || warp * 512 + r * 32 + lane < ne) {
+      const uint32_t band = rk[r] >> 22;
+      const uint32_t pos = boff[band] + hist[warp * nbp + band] + ((rk[r] >> 13) & 0x1ffu);
+      sbuf[pos] = make_uint2(__ldg(tlo + 4 * 32 * r), (rk[r] & 0xfffu) | ((rk[r] & 0x1000u) << 19));
     }
   }
   if (threadIdx.x == 0) {
@@ -209,12 +212,23 @@ __global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs
     for (int r = 0; r < 16; ++r) {
       const int i = warp * 512 + r * 32 + lane;
       if (i < ne) {
-        const uint32_t band = rk[r] >> 16;
-        const uint32_t pos = boff[band] + hist[warp * nbp + band] + (rk[r] & 0xffffu);
+        const uint32_t band = rk[r] >> 22;
+        const uint32_t pos = boff[band] + hist[warp * nbp + band] + ((rk[r] >> 13) & 0x1ffu);
         a.wide_t[e0 + pos] = ev[i].t_us;
       }
     }
   }
+}
+
+template <bool RANK_ATOMIC>
+__global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  // Chunk entirely after the last frame of this render: nothing to integrate.
+  if (a.ev[0].t_us > a.t_cap) return;
+  const int tile = blockIdx.x;
+  const int ne = (int)min((int64_t)kTile, a.n - (int64_t)tile * kTile);
+  if (ne == kTile) partition_tile<RANK_ATOMIC, true>(a, smem, tile, ne);
+  else partition_tile<RANK_ATOMIC, false>(a, smem, tile, ne);
 }
 
 template <bool RA>
