@@ -19,7 +19,7 @@
 namespace esi {
 
 size_t partition_smem_bytes(int nb) {
-  const int nbp = (nb + 1) & ~1;
+  const int nbp = (nb + 7) & ~7;
   return (size_t)kTile * sizeof(uint2) + (size_t)kPartWarps * nbp * sizeof(uint16_t) +
          (size_t)(nb + 1) * sizeof(uint32_t) + 64 * sizeof(uint32_t);
 }
@@ -75,7 +75,7 @@ __device__ __forceinline__ uint32_t pack_rk(uint32_t pix, bool neg, uint32_t ran
 // FULL: the tile holds kTile events (no bounds checks on the common path).
 template <bool RANK_ATOMIC, bool FULL>
 __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char* smem, int tile, int ne) {
-  const int nbp = (a.nb + 1) & ~1;
+  const int nbp = (a.nb + 7) & ~7;
   uint2* sbuf = reinterpret_cast<uint2*>(smem);
   uint16_t* hist = reinterpret_cast<uint16_t*>(sbuf + kTile);    // [kPartWarps][nbp]
   uint32_t* boff = reinterpret_cast<uint32_t*>(hist + kPartWarps * nbp);  // [nb + 1]
@@ -87,7 +87,8 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   const esi_event_t* ev = a.ev + e0;
   const int4* evw = reinterpret_cast<const int4*>(ev) + warp * 512 + lane;   // this lane's first event
 
-  for (int i = threadIdx.x; i < kPartWarps * nbp; i += kPartThreads) hist[i] = 0;
+  for (int i = threadIdx.x; i < kPartWarps * nbp / 8; i += kPartThreads)
+    reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
   // t of the event preceding this warp's first event (later rounds take it from lane 31)
   int64_t t_before = 0;
   if (lane == 0 && (FULL || warp * 512 < ne)) {
@@ -199,13 +200,20 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     s_wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
     a.tile_wide[tile] = s_wide;
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
 
-  uint4* dst = reinterpret_cast<uint4*>(a.rec + e0);
-  const uint4* src = reinterpret_cast<const uint4*>(sbuf);
-  const int n2 = ne >> 1;
-  for (int i = threadIdx.x; i < n2; i += kPartThreads) dst[i] = src[i];
-  if ((ne & 1) && threadIdx.x == 0) a.rec[e0 + ne - 1] = sbuf[ne - 1];
+  // sorted tile -> global with one TMA bulk copy (async proxy; the generic-proxy
+  // shared-memory writes above were fenced by every writer before the barrier)
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)(ne & ~1) * 8u;
+    if (bytes) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(a.rec + e0), "r"((uint32_t)__cvta_generic_to_shared(sbuf)), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (ne & 1) a.rec[e0 + ne - 1] = sbuf[ne - 1];
+  }
 
   if (s_wide) {  // rare: tile spans >= 2^32 us; keep the full timestamps beside the records
 #pragma unroll
@@ -218,6 +226,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
       }
     }
   }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // copy complete before the CTA retires
 }
 
 template <bool RANK_ATOMIC>

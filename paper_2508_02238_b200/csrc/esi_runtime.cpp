@@ -571,6 +571,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     }
     ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_first, hcf, nc * sizeof(void*), cudaMemcpyHostToDevice, st));
     ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_n, hcn, nc * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    h->st_launches += 1;   // plan
     ESI_CUDA(h, launch_plan(h->d_chunk_first, h->d_chunk_n, (int)nc, h->d_tf, (int)F, t_cap,
                             h->allow_fast ? 1 : 0, h->d_info, h->d_n_active, st));
     int32_t* hna = (int32_t*)(h->h_pin + nc * 16 + 16);
