@@ -119,7 +119,7 @@ constexpr int kSlots = 8;   // events of one pixel in one segment applied by a s
 constexpr uint32_t kEmpty = 0xffffu;
 constexpr int kNW = 16;                       // warps per CTA
 constexpr int kNT = kNW * 32;                 // threads per CTA
-constexpr int kEPT = 2;                       // events per thread per segment
+constexpr int kEPT = 4;                       // events per thread per segment
 constexpr int kSB = kNT * kEPT;               // events per sub-batch
 
 // Shared memory of one CTA, carved at run time (the band size is a run-time
@@ -349,13 +349,13 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
   }
 }
 
-// number of sub-batch events in [0, n) with relative time <= tj (times sorted, n <= 1024):
-// warp-wide 2-level 32-ary search, identical in every warp (no barrier needed)
+// number of sub-batch events in [0, n) with relative time <= tj (times sorted, n <= kSB):
+// warp-wide 32-ary search, identical in every warp (no barrier needed)
 __device__ __forceinline__ int upper_bound_rel(const uint2* sub, int n, uint32_t trel, int32_t tj, int lane) {
-  static_assert(kSB <= 1024, "2-level search");
+  static_assert(kSB <= 32768, "3-level search");
   int lo = 0;
 #pragma unroll
-  for (int stride = 32; stride >= 1; stride >>= 5) {
+  for (int stride = kSB > 1024 ? 1024 : 32; stride >= 1; stride >>= 5) {
     const int p = lo + lane * stride;
     const bool le = p < n && (int32_t)(sub[p].x - trel) <= tj;
     const unsigned b = __ballot_sync(kFull, le);
