@@ -378,3 +378,19 @@ def test_c4_full_size_sampled():
     assert_state_close(S.reshape(-1)[pix], T.reshape(-1)[pix], S_ref[0], T_ref[0])
     # every pixel: frame values in range, state within the clamp bounds
     assert float(np.abs(S).max()) <= w.params["s_max"] + 1e-6
+
+
+def test_c2_at_1000_fps():
+    """1000 FPS readout (BASELINE config 4 renders at 100 and 1000 FPS): 10x more
+    frame windows per chunk, mostly near-empty (the sparse-window path)."""
+    from esi_synth import frame_times
+    w = wl("c2", duration_us=300_000)
+    tf = frame_times(300_000, 1000)
+    check(w.W, w.H, ev_np_of(w), tf, w.params)
+
+
+def test_c3_full_length_hot_pixels_dense_path():
+    """Config 3 over its full 5 s: hot-pixel bursts put many events of one pixel in
+    one frame window (chain and dense paths)."""
+    w = wl("c3")
+    check(w.W, w.H, ev_np_of(w), w.t_frames, w.params)
