@@ -100,6 +100,7 @@ struct esi_handle {
   int64_t st_launches = 0, st_events = 0, st_chunks = 0, st_fast = 0;
   bool atomic_rank = true;   // K1 ranks from lane-ordered smem atomics (probed at create)
   bool allow_fast = true;    // K2 fast variant allowed (dt_cut < 2^23)
+  bool single_stream = false; // ESI_SINGLE_STREAM=1: K1 and K2 on one stream
 };
 
 namespace {
@@ -379,6 +380,7 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   if (!rc) rc = ensure_pinned(h, 1 << 16);
   if (!rc) rc = esi_reset(h);
   h->allow_fast = h->dp.dt_cut < ((int64_t)1 << 23) && !getenv("ESI_DISABLE_FAST");
+  h->single_stream = getenv("ESI_SINGLE_STREAM") && atoi(getenv("ESI_SINGLE_STREAM")) != 0;
   if (!rc) {
     // K1 rank mode: probe that warp-wide smem atomics serve same-address lanes in lane order
     const char* mode = getenv("ESI_RANK_MODE");
@@ -584,12 +586,17 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
 
     // K1 runs on the aux stream, K2 on the handle's stream; chunk c uses buffer c & 1:
     // K1(c) waits for the render's setup and for K2(c-2); K2(c) waits for K1(c).
-    ESI_CUDA(h, cudaEventRecord(h->ev_start, st));
-    ESI_CUDA(h, cudaStreamWaitEvent(h->aux, h->ev_start, 0));
+    // (ESI_SINGLE_STREAM=1: both kernels on the handle's stream, no cross-stream events)
+    const bool two = !h->single_stream;
+    cudaStream_t k1s = two ? h->aux : st;
+    if (two) {
+      ESI_CUDA(h, cudaEventRecord(h->ev_start, st));
+      ESI_CUDA(h, cudaStreamWaitEvent(h->aux, h->ev_start, 0));
+    }
     int64_t index_base = 0;
     for (int c = 0; c < n_act; ++c) {
       const int bf = c & 1;
-      if (c >= 2) ESI_CUDA(h, cudaStreamWaitEvent(h->aux, h->ev_k2[bf], 0));
+      if (two && c >= 2) ESI_CUDA(h, cudaStreamWaitEvent(h->aux, h->ev_k2[bf], 0));
       const Chunk& ch = chunks[c];
       const int n_tiles = (int)((ch.n + kTile - 1) / kTile);
       PartArgs pa;
@@ -613,11 +620,13 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.wide_t = h->wide_t[bf];
       pa.err = h->d_err;
       TimedLaunch t1;
-      timed_begin(h, 0, &t1, h->aux);
-      ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, h->aux));
+      timed_begin(h, 0, &t1, k1s);
+      ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, k1s));
       timed_end(h, &t1);
-      ESI_CUDA(h, cudaEventRecord(h->ev_k1[bf], h->aux));
-      ESI_CUDA(h, cudaStreamWaitEvent(st, h->ev_k1[bf], 0));
+      if (two) {
+        ESI_CUDA(h, cudaEventRecord(h->ev_k1[bf], h->aux));
+        ESI_CUDA(h, cudaStreamWaitEvent(st, h->ev_k1[bf], 0));
+      }
 
       IntArgs ia;
       ia.info = h->d_info + c;
@@ -649,7 +658,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
         ESI_CUDA(h, launch_integrate(ia, st));
       }
       timed_end(h, &t2);
-      ESI_CUDA(h, cudaEventRecord(h->ev_k2[bf], st));
+      if (two) ESI_CUDA(h, cudaEventRecord(h->ev_k2[bf], st));
       h->st_launches += 2;
       h->st_chunks += 1;
       index_base += ch.n;
