@@ -272,24 +272,30 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
                                                 uint32_t gen, int warp, int lane, const FastConst& k) {
   const int tid = threadIdx.x;
   const uint32_t tag = gen << 16;
-  for (int i = e0 + tid; i < e1; i += kNT) {              // claim
-    const int px = (int)(sub[i].y & 0x7fffffffu);
-    const uint32_t old = atomicExch(&sm.head[px], tag | (uint32_t)(i - e0));
-    sm.next[i - e0] = (old & 0xffff0000u) == tag ? (uint16_t)old : (uint16_t)kEmpty;
+  uint2 evr[kEPT];                                        // this thread's events, kept from claim to apply
+#pragma unroll
+  for (int r = 0; r < kEPT; ++r) {                        // claim
+    const int i = e0 + tid + r * kNT;
+    if (i < e1) {
+      evr[r] = sub[i];
+      const int px = (int)(evr[r].y & 0x7fffffffu);
+      const uint32_t old = atomicExch(&sm.head[px], tag | (uint32_t)(i - e0));
+      sm.next[i - e0] = (old & 0xffff0000u) == tag ? (uint16_t)old : (uint16_t)kEmpty;
+    }
   }
   __syncthreads();
   uint32_t* wl = reinterpret_cast<uint32_t*>(sm.stage + warp * 64);   // <= kEPT * 32 chain heads
   int nch = 0;
-  for (int ib = e0; ib < e1; ib += kNT) {                 // apply: singles now, chains deferred
-    const int i = ib + tid;
+#pragma unroll
+  for (int r = 0; r < kEPT; ++r) {                        // apply: singles now, chains deferred
+    if (e0 + r * kNT >= e1) break;                        // uniform: no thread has an event in this round
+    const int i = e0 + tid + r * kNT;
     bool chain = false;
-    uint32_t me = 0;
+    const uint32_t me = (uint32_t)(i - e0);
     if (i < e1) {
-      const uint2 ev = sub[i];
-      const int px = (int)(ev.y & 0x7fffffffu);
-      me = (uint32_t)(i - e0);
+      const int px = (int)(evr[r].y & 0x7fffffffu);
       if (sm.head[px] == (tag | me)) {
-        if (sm.next[me] == kEmpty) apply_event<BM>(sm.S, sm.T, px, ev, trel, k);
+        if (sm.next[me] == kEmpty) apply_event<BM>(sm.S, sm.T, px, evr[r], trel, k);
         else chain = true;
       }
     }
