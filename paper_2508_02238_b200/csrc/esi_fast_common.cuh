@@ -1,0 +1,185 @@
+// esi_fast_common.cuh -- arithmetic shared by the two K2 variants of the fast
+// (32-bit relative time) path: decay (Eq. 4), clamp (Eq. 13), readout (Eq. 14),
+// the Alg. 2 event body, the dense-pixel warp scan of clamped affine maps, and
+// small copy/search helpers.  Included inside namespace esi { namespace { ... } }.
+#pragma once
+
+constexpr int kSlots = 8;   // events of one pixel in one segment applied by a single thread
+constexpr uint32_t kEmpty = 0xffffu;
+
+constexpr float kMagic = 8388608.0f;   // 2^23
+
+struct FastConst {
+  float tau_h, tau_l;                  // tau = 1e6/k us = tau_h + tau_l
+  float kh, kl, k_tau_l;               // k_us = kh + kl (no systematic bias), k_us * tau_l
+  float b;
+  float C, smin, smax;
+  float scale, off_frac, magic_off;    // map: byte = low8(bits(rd(v*scale + off_frac + 2^23 + off_int)))
+  float scale_w2;                      // k_us^2 * scale: Eq. 14 of S*(k w)^2 with k^2 folded in
+  int32_t tau_int;                     // tau is an integer (tau_l == 0)
+  int32_t fold;                        // readout mode: 1 = folded (b = 2, readout decay, no clamp, integer tau)
+  int32_t rd, cl;                      // readout decay; readout clamp needed (bounds exclude 0)
+};
+
+__device__ __forceinline__ FastConst make_const(const IntArgs& a) {
+  FastConst c;
+  c.tau_h = a.dp.tau_h;
+  c.tau_l = a.dp.tau_l;
+  c.kh = a.dp.kh;
+  c.kl = a.dp.kl;
+  c.k_tau_l = a.dp.kf * a.dp.tau_l;
+  c.b = a.dp.b;
+  c.C = a.mp.C;
+  c.smin = a.mp.smin;
+  c.smax = a.mp.smax;
+  c.scale = a.mp.scale;
+  c.off_frac = a.mp.off_frac;
+  c.magic_off = kMagic + (float)a.mp.off_int;
+  c.scale_w2 = a.mp.scale_w2;
+  c.tau_int = a.dp.tau_l == 0.f;
+  c.rd = a.mp.readout_decay != 0;
+  c.cl = !(a.mp.smin <= 0.f && a.mp.smax >= 0.f);
+  c.fold = a.dp.bmode == 2 && c.rd && !c.cl && c.tau_int;
+  return c;
+}
+
+// Eq. 4: u = 1 - k dt computed as k ((tau_h - dt) + tau_l) with the
+// float pair kh + kl = k * 1e-6 /us.  tau_h - dt is exact near the cutoff, so
+// u keeps its relative precision there and u <= 0 exactly when dt >= ceil(tau)
+// (reading A14); the pair keeps the product free of a systematic bias (a
+// single-float k would bias every decay factor by the same ~3e-8 relative).
+__device__ __forceinline__ float decay_u(float dt, const FastConst& c) {
+  const float w = (c.tau_h - dt) + c.tau_l;
+  return fmaxf(fmaf(c.kh, w, c.kl * w), 0.f);
+}
+
+template <int BM>
+__device__ __forceinline__ float ev_decay(float dt, const FastConst& c) {
+  const float u = decay_u(dt, c);
+  if (BM == 2) return u * u;
+  return exp2f(c.b * __log2f(u));      // log2(0) = -inf -> d = 0
+}
+
+// Eq. 13 clamp of one event's result.
+__device__ __forceinline__ float clampS(float s, const FastConst& c) { return fminf(fmaxf(s, c.smin), c.smax); }
+
+// Readout of 2 pixels (reading A4: v = S d(t_j - T), non-mutating; Eq. 13 clamp
+// when the bounds exclude 0; Eq. 14 rounded half away from zero, reading A8).
+// Folded mode (b = 2, integer tau, bounds containing 0): with w = T - (t_j - tau)
+// = tau - dt (exact), d = (k w)^2 for w > 0 and 0 otherwise, so
+//   x = S w^2 (k^2 scale) + off_frac   -- 4 packed f32x2 ops + 2 max per 2 pixels.
+template <int BM>
+__device__ __forceinline__ uint32_t readout2(float2 s, float2 T, float tj, float aj, const FastConst& c) {
+  float2 x;
+  if (c.fold) {
+    float2 w = __fadd2_rn(T, make_float2(-aj, -aj));                          // tau - dt, exact
+    w.x = fmaxf(w.x, 0.f);
+    w.y = fmaxf(w.y, 0.f);
+    const float2 v = __fmul2_rn(s, __fmul2_rn(w, w));
+    x = __ffma2_rn(v, make_float2(c.scale_w2, c.scale_w2), make_float2(c.off_frac, c.off_frac));
+  } else {
+    float2 v = s;
+    if (c.rd) {
+      const float dx = decay_u(tj - T.x, c), dy = decay_u(tj - T.y, c);
+      float2 d;
+      if (BM == 2) d = make_float2(dx * dx, dy * dy);
+      else d = make_float2(exp2f(c.b * __log2f(dx)), exp2f(c.b * __log2f(dy)));
+      v = __fmul2_rn(s, d);
+    }
+    if (c.cl) {
+      v.x = fminf(fmaxf(v.x, c.smin), c.smax);
+      v.y = fminf(fmaxf(v.y, c.smin), c.smax);
+    }
+    x = __ffma2_rn(v, make_float2(c.scale, c.scale), make_float2(c.off_frac, c.off_frac));
+  }
+  const float2 r = __fadd2_rd(x, make_float2(c.magic_off, c.magic_off));   // 2^23 + off_int + floor(x)
+  return __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x0040);  // 2 bytes in the low half
+}
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Alg. 2 loop body for one event of pixel px, sequentially.
+template <int BM>
+__device__ __forceinline__ void apply_event(float* S, float* T, int px, uint2 ev, uint32_t trel,
+                                            const FastConst& k) {
+  const float te = (float)(int32_t)(ev.x - trel);
+  const float pc = ((int32_t)ev.y < 0) ? -k.C : k.C;
+  float s = S[px] + pc;                                   // S <- S + p C
+  s *= ev_decay<BM>(te - T[px], k);                       // S <- S max{(1 - k dt)^b, 0}
+  S[px] = clampS(s, k);                                   // S <- min(max(S, S_min), S_max)
+  T[px] = te;                                             // T <- t
+}
+
+// Dense pixel (> kSlots events in the segment): one warp composes the events'
+// clamped affine maps s -> clamp(a s + c, lo, hi), a >= 0:
+// event i is f_i = (d_i, d_i p_i C, S_min, S_max) and
+//   F o G = (aF aG, aF cG + cF, clamp(aF loG + cF, loF, hiF), clamp(aF hiG + cF, loF, hiF)).
+// The segment is scanned 32 events at a time; the pixel's events of each group
+// are compacted to the low lanes (arrival order), their maps are combined by a
+// warp-shuffle inclusive scan, and the last prefix is applied to the state.
+template <int BM>
+__device__ __forceinline__ void dense_pixel_apply(float* S, float* T, const uint2* sub, uint2* stage, int e0,
+                                                  int e1, int q, uint32_t trel, int lane, const FastConst& k) {
+  float s = S[q], tprev = T[q];
+  for (int base = e0; base < e1; base += 32) {
+    const int i = base + lane;
+    const uint2 ev = i < e1 ? sub[i] : make_uint2(0u, 0xffffffffu);
+    const bool mine = i < e1 && (int)(ev.y & 0x7fffffffu) == q;
+    const unsigned m = __ballot_sync(kFull, mine);
+    if (!m) continue;
+    const int nk = __popc(m);
+    if (mine) stage[__popc(m & lanemask_lt())] = ev;     // compact, arrival order kept
+    __syncwarp();
+    const uint2 cev = stage[lane];
+    __syncwarp();
+    const float te = (float)(int32_t)(cev.x - trel);
+    float tp = __shfl_up_sync(kFull, te, 1);
+    if (lane == 0) tp = tprev;
+    const bool act = lane < nk;
+    const float d = act ? ev_decay<BM>(te - tp, k) : 1.f;
+    const float pc = ((int32_t)cev.y < 0) ? -k.C : k.C;
+    float fa = d, fc = act ? d * pc : 0.f, flo = k.smin, fhi = k.smax;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float ga = __shfl_up_sync(kFull, fa, off), gc = __shfl_up_sync(kFull, fc, off);
+      const float glo = __shfl_up_sync(kFull, flo, off), ghi = __shfl_up_sync(kFull, fhi, off);
+      if (lane >= off) {                                  // F <- F o G (G = earlier events)
+        const float nlo = fminf(fmaxf(fmaf(fa, glo, fc), flo), fhi);
+        const float nhi = fminf(fmaxf(fmaf(fa, ghi, fc), flo), fhi);
+        fc = fmaf(fa, gc, fc);
+        fa = fa * ga;
+        flo = nlo;
+        fhi = nhi;
+      }
+    }
+    const float La = __shfl_sync(kFull, fa, nk - 1), Lc = __shfl_sync(kFull, fc, nk - 1);
+    const float Llo = __shfl_sync(kFull, flo, nk - 1), Lhi = __shfl_sync(kFull, fhi, nk - 1);
+    s = fminf(fmaxf(fmaf(La, s, Lc), Llo), Lhi);
+    tprev = __shfl_sync(kFull, te, nk - 1);
+  }
+  if (lane == 0) {
+    S[q] = s;
+    T[q] = tprev;
+  }
+}
+
+// number of sub-batch events in [0, n) with relative time <= tj (times sorted, n <= kSB):
+// warp-wide 32-ary search, identical in every warp (no barrier needed)
+template <int SB>
+__device__ __forceinline__ int upper_bound_rel(const uint2* sub, int n, uint32_t trel, int32_t tj, int lane) {
+  int lo = 0;
+#pragma unroll
+  for (int stride = SB > 1024 ? 1024 : 32; stride >= 1; stride >>= 5) {
+    const int p = lo + lane * stride;
+    const bool le = p < n && (int32_t)(sub[p].x - trel) <= tj;
+    const unsigned b = __ballot_sync(kFull, le);
+    if (b == 0u) return lo;                               // sub[lo] > tj (lo is always a candidate)
+    lo += (31 - __clz(b)) * stride;
+  }
+  return lo + 1;
+}
+
