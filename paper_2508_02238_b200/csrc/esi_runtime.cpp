@@ -101,7 +101,6 @@ struct esi_handle {
   bool atomic_rank = true;   // K1 ranks from lane-ordered smem atomics (probed at create)
   bool allow_fast = true;    // K2 fast variant allowed (dt_cut < 2^23)
   bool single_stream = false; // ESI_SINGLE_STREAM=1: K1 and K2 on one stream
-  bool k2_warp = false;       // fast K2 variant: warp-autonomous (ESI_K2=warp) or block segments
 };
 
 namespace {
@@ -382,7 +381,6 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   if (!rc) rc = esi_reset(h);
   h->allow_fast = h->dp.dt_cut < ((int64_t)1 << 23) && !getenv("ESI_DISABLE_FAST");
   h->single_stream = getenv("ESI_SINGLE_STREAM") && atoi(getenv("ESI_SINGLE_STREAM")) != 0;
-  h->k2_warp = getenv("ESI_K2") && strcmp(getenv("ESI_K2"), "warp") == 0;
   if (!rc) {
     // K1 rank mode: probe that warp-wide smem atomics serve same-address lanes in lane order
     const char* mode = getenv("ESI_RANK_MODE");
@@ -654,7 +652,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       TimedLaunch t2;
       timed_begin(h, 1, &t2);
       if (hinfo[c].fast) {
-        ESI_CUDA(h, h->k2_warp ? launch_integrate_warp(ia, st) : launch_integrate_fast(ia, st));
+        ESI_CUDA(h, launch_integrate_fast(ia, st));
         h->st_fast += 1;
       } else {
         ESI_CUDA(h, launch_integrate(ia, st));
