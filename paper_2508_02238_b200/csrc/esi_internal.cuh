@@ -18,8 +18,8 @@
 
 namespace esi {
 
-constexpr int kTile = 8192;          // events per partition tile
-constexpr int kPartThreads = 512;    // 16 warps x 16 events per thread
+constexpr int kTile = 4096;          // events per partition tile
+constexpr int kPartThreads = 512;    // 16 warps x 8 events per thread
 constexpr int kPartWarps = kPartThreads / 32;
 constexpr int kSubBatch = 1024;      // band events staged in smem per sub-batch
 constexpr int kMaxTilesPerChunk = 1024;

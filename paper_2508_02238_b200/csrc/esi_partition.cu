@@ -20,7 +20,7 @@ namespace esi {
 
 size_t partition_smem_bytes(int nb) {
   const int nbp = (nb + 7) & ~7;
-  return (size_t)kTile * sizeof(uint2) + (size_t)kPartWarps * nbp * sizeof(uint16_t) +
+  return (size_t)kTile * sizeof(int4) + (size_t)kPartWarps * nbp * sizeof(uint16_t) +
          (size_t)(nb + 1) * sizeof(uint32_t) + 64 * sizeof(uint32_t);
 }
 
@@ -73,98 +73,102 @@ __device__ __forceinline__ uint32_t pack_rk(uint32_t pix, bool neg, uint32_t ran
 // order, which esi_probe_atomic_order checks at esi_create; otherwise ranks come
 // from a ballot multi-split over the band bits (order by construction).
 // FULL: the tile holds kTile events (no bounds checks on the common path).
+//
+// The tile's raw 16-B records are staged in shared memory with cp.async (every
+// load of the tile in flight at once); the sorted tile later reuses the first
+// half of that buffer, after the records have been consumed into registers.
 template <bool RANK_ATOMIC, bool FULL>
 __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char* smem, int tile, int ne) {
+  constexpr int EPT = kTile / kPartThreads;                      // events per thread (8)
+  constexpr int WEV = EPT * 32;                                  // events per warp (256)
   const int nbp = (a.nb + 7) & ~7;
-  uint2* sbuf = reinterpret_cast<uint2*>(smem);
-  uint16_t* hist = reinterpret_cast<uint16_t*>(sbuf + kTile);    // [kPartWarps][nbp]
+  int4* raw = reinterpret_cast<int4*>(smem);                     // [kTile] staged records
+  uint2* sbuf = reinterpret_cast<uint2*>(smem);                  // [kTile] sorted records (aliases raw)
+  uint16_t* hist = reinterpret_cast<uint16_t*>(raw + kTile);     // [kPartWarps][nbp]
   uint32_t* boff = reinterpret_cast<uint32_t*>(hist + kPartWarps * nbp);  // [nb + 1]
   uint32_t* wsum = boff + a.nb + 1;                               // [64]
   __shared__ int s_wide;
+  __shared__ int64_t s_tprev;
 
   const int64_t e0 = (int64_t)tile * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const esi_event_t* ev = a.ev + e0;
-  const int4* evw = reinterpret_cast<const int4*>(ev) + warp * 512 + lane;   // this lane's first event
+  const int4* evv = reinterpret_cast<const int4*>(ev);
 
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = warp * WEV + r * 32 + lane;
+    if (FULL || i < ne) {
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(raw + i);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(evv + i) : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int i = threadIdx.x; i < kPartWarps * nbp / 8; i += kPartThreads)
     reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
-  // t of the event preceding this warp's first event (later rounds take it from lane 31)
-  int64_t t_before = 0;
-  if (lane == 0 && (FULL || warp * 512 < ne)) {
-    const int i0 = warp * 512;
-    t_before = (i0 > 0) ? ev[i0 - 1].t_us : (tile > 0 ? ev[-1].t_us : *a.prev_t);
-  }
+  if (threadIdx.x == 0) s_tprev = tile > 0 ? ev[-1].t_us : *a.prev_t;   // predecessor of the tile's first event
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 
   uint16_t* myhist = hist + warp * nbp;
-  uint32_t rk[16];   // t is re-read (L2) at the scatter: keeps the ranking loop within 64 registers
+  uint32_t rk[EPT], tl[EPT];
   const uint32_t W = (uint32_t)a.W, H = (uint32_t)a.H, BPX = (uint32_t)a.band_px;
   const int64_t t_min = a.t_min;
+  const int64_t tprev0 = s_tprev;
 
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    int4 raw[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = g * 4 + u;
-      raw[u] = (FULL || warp * 512 + r * 32 + lane < ne) ? ld_stream16(evw + r * 32) : make_int4(0, 0, 0, 0);
+  for (int r = 0; r < EPT; ++r) {
+    const int i = warp * WEV + r * 32 + lane;
+    const bool act = FULL || i < ne;
+    const int4 rw = act ? raw[i] : make_int4(0, 0, 0, 0);
+    const int64_t t = (int64_t)(((uint64_t)(uint32_t)rw.y << 32) | (uint32_t)rw.x);
+    uint32_t x = (uint32_t)rw.z & 0xffffu;
+    uint32_t y = (uint32_t)rw.z >> 16;
+    const int p = (int)(int8_t)(rw.w & 0xff);
+    const int64_t tp = i > 0 ? *reinterpret_cast<const int64_t*>(raw + i - 1) : tprev0;
+    // validation (reading A15), one combined test on the common path
+    const bool bad = (x >= W) | (y >= H) | (p * p != 1) | (t < t_min) | (t < tp);
+    if (act && bad) {
+      int code;
+      if (x >= W || y >= H) code = ESI_ERR_OUT_OF_BOUNDS;
+      else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
+      else code = ESI_ERR_NEGATIVE_INTERVAL;
+      atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + i) << 8) | (unsigned)code);
+      x = 0; y = 0;              // keep the pipeline well-defined; the call reports the error
     }
+    const uint32_t pid = y * W + x;
+    const uint32_t band = act ? (uint32_t)(((uint64_t)pid * a.band_magic) >> 40) : 0u;
+    const uint32_t pix = pid - band * BPX;
+    uint32_t rank;
+    if (RANK_ATOMIC) {
+      uint32_t* hw = reinterpret_cast<uint32_t*>(myhist);
+      const uint32_t sh = (band & 1u) << 4;
+      const uint32_t old = act ? atomicAdd(hw + (band >> 1), 1u << sh) : 0u;
+      rank = (old >> sh) & 0xffffu;
+    } else {
+      // warp multi-split: lanes whose band equals mine
+      unsigned peers = __ballot_sync(kFull, act);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = g * 4 + u;
-      const bool act = FULL || warp * 512 + r * 32 + lane < ne;
-      const int64_t t = (int64_t)(((uint64_t)(uint32_t)raw[u].y << 32) | (uint32_t)raw[u].x);
-      uint32_t x = (uint32_t)raw[u].z & 0xffffu;
-      uint32_t y = (uint32_t)raw[u].z >> 16;
-      const int p = (int)(int8_t)(raw[u].w & 0xff);
-      int64_t tp = __shfl_up_sync(kFull, t, 1);
-      if (lane == 0) tp = t_before;
-      t_before = __shfl_sync(kFull, t, 31);
-      // validation (reading A15), one combined test on the common path
-      const bool bad = (x >= W) | (y >= H) | (p * p != 1) | (t < t_min) | (t < tp);
-      if (act && bad) {
-        int code;
-        if (x >= W || y >= H) code = ESI_ERR_OUT_OF_BOUNDS;
-        else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
-        else code = ESI_ERR_NEGATIVE_INTERVAL;
-        atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + warp * 512 + r * 32 + lane) << 8) |
-                             (unsigned)code);
-        x = 0; y = 0;            // keep the pipeline well-defined; the call reports the error
+      for (int bit = 0; bit < 10; ++bit) {   // nb <= 1024
+        const bool bset = (band >> bit) & 1u;
+        const unsigned bb = __ballot_sync(kFull, bset);
+        peers &= bset ? bb : ~bb;
       }
-      const uint32_t pid = y * W + x;
-      const uint32_t band = act ? (uint32_t)(((uint64_t)pid * a.band_magic) >> 40) : 0u;
-      const uint32_t pix = pid - band * BPX;
-      uint32_t rank;
-      if (RANK_ATOMIC) {
-        uint32_t* hw = reinterpret_cast<uint32_t*>(myhist);
-        const uint32_t sh = (band & 1u) << 4;
-        const uint32_t old = act ? atomicAdd(hw + (band >> 1), 1u << sh) : 0u;
-        rank = (old >> sh) & 0xffffu;
-      } else {
-        // warp multi-split: lanes whose band equals mine
-        unsigned peers = __ballot_sync(kFull, act);
-#pragma unroll
-        for (int bit = 0; bit < 10; ++bit) {   // nb <= 1024
-          const bool bset = (band >> bit) & 1u;
-          const unsigned bb = __ballot_sync(kFull, bset);
-          peers &= bset ? bb : ~bb;
-        }
-        if (!act) peers = 0u;
-        const uint32_t rl = __popc(peers & lanemask_lt());
-        uint32_t base = 0;
-        if (act && rl == 0) {
-          base = myhist[band];
-          myhist[band] = (uint16_t)(base + __popc(peers));
-        }
-        base = __shfl_sync(kFull, base, act ? (__ffs(peers) - 1) : lane);
-        __syncwarp();
-        rank = base + rl;
+      if (!act) peers = 0u;
+      const uint32_t rl = __popc(peers & lanemask_lt());
+      uint32_t base = 0;
+      if (act && rl == 0) {
+        base = myhist[band];
+        myhist[band] = (uint16_t)(base + __popc(peers));
       }
-      rk[r] = pack_rk(pix, p < 0 && !(act && bad), rank, band);
+      base = __shfl_sync(kFull, base, act ? (__ffs(peers) - 1) : lane);
+      __syncwarp();
+      rank = base + rl;
     }
+    tl[r] = (uint32_t)t;
+    rk[r] = pack_rk(pix, p < 0 && !(act && bad), rank, band);
   }
-  __syncthreads();
+  __syncthreads();                               // raw consumed: its first half becomes sbuf
 
   // per band: exclusive prefix over the warps, band total into boff[band]
   for (int b = threadIdx.x; b < a.nb; b += kPartThreads) {
@@ -185,13 +189,12 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     const uint32_t cnt = boff[b + 1] - boff[b];
     a.meta[(int64_t)b * gridDim.x + tile] = boff[b] | (cnt << 16);
   }
-  const uint32_t* tlo = reinterpret_cast<const uint32_t*>(ev) + 4 * (warp * 512 + lane);   // low words of t
 #pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    if (FULL || warp * 512 + r * 32 + lane < ne) {
+  for (int r = 0; r < EPT; ++r) {
+    if (FULL || warp * WEV + r * 32 + lane < ne) {
       const uint32_t band = rk[r] >> 22;
       const uint32_t pos = boff[band] + hist[warp * nbp + band] + ((rk[r] >> 13) & 0x1ffu);
-      sbuf[pos] = make_uint2(__ldg(tlo + 4 * 32 * r), (rk[r] & 0xfffu) | ((rk[r] & 0x1000u) << 19));
+      sbuf[pos] = make_uint2(tl[r], (rk[r] & 0xfffu) | ((rk[r] & 0x1000u) << 19));
     }
   }
   if (threadIdx.x == 0) {
@@ -217,8 +220,8 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
 
   if (s_wide) {  // rare: tile spans >= 2^32 us; keep the full timestamps beside the records
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const int i = warp * 512 + r * 32 + lane;
+    for (int r = 0; r < EPT; ++r) {
+      const int i = warp * WEV + r * 32 + lane;
       if (i < ne) {
         const uint32_t band = rk[r] >> 22;
         const uint32_t pos = boff[band] + hist[warp * nbp + band] + ((rk[r] >> 13) & 0x1ffu);
@@ -230,7 +233,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
 }
 
 template <bool RANK_ATOMIC>
-__global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs a) {
+__global__ void __launch_bounds__(kPartThreads, 3) esi_partition_kernel(PartArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   // Chunk entirely after the last frame of this render: nothing to integrate.
   if (a.ev[0].t_us > a.t_cap) return;
