@@ -36,7 +36,7 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, out: str = None, objdir: str = None) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, objdir: str = None, extra=()) -> str:
     if out is None and not force and not needs_build():
         return LIB
     lib = out or LIB
@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, objdir: s
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
-        cmd = [nvcc, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c",
+        cmd = [nvcc, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd[1:1] = ["-x", "cu"]
@@ -60,5 +60,17 @@ def build(force: bool = False, verbose: bool = False, out: str = None, objdir: s
     return lib
 
 
+CHECKED_LIB = os.path.join(HERE, "libesi_checked.so")
+
+
+def build_checked() -> str:
+    """Build with device-side invariant checks (ESI_DCHECK) -> libesi_checked.so;
+    select it with ESI_LIB_PATH for a checked test run."""
+    return build(out=CHECKED_LIB, objdir=os.path.join(HERE, "build_checked"), extra=("-DESI_DEBUG_CHECKS",))
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--checked" in sys.argv:
+        print(build_checked())
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

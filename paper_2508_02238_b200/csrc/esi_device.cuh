@@ -1,11 +1,29 @@
 // esi_device.cuh -- small device helpers shared by the libesi kernels.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include "esi_internal.cuh"
 
 namespace esi {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// Device-side invariant checks, compiled in only for the checked build
+// (python -m paper_2508_02238_b200.build --checked -> libesi_checked.so); a failed
+// check prints its location and traps (the render call then reports ESI_ERR_CUDA).
+#ifdef ESI_DEBUG_CHECKS
+#define ESI_DCHECK(c)                                                              \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("ESI_DCHECK failed: %s at %s:%d\n", #c, __FILE__, __LINE__);          \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define ESI_DCHECK(c) \
+  do {                \
+  } while (0)
+#endif
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

@@ -112,7 +112,7 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
 // or re-claims.
 template <int BM>
 __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* sub, int e0, int e1, uint32_t trel,
-                                                uint32_t gen, int warp, int lane, const FastConst& k) {
+                                                uint32_t gen, int warp, int lane, const FastConst& k, int a_bp) {
   const int tid = threadIdx.x;
   const uint32_t tag = gen << 16;
   uint2 evr[kEPT];                                        // this thread's events, kept from claim to apply
@@ -122,6 +122,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
     if (i < e1) {
       evr[r] = sub[i];
       const int px = (int)(evr[r].y & 0x7fffffffu);
+      ESI_DCHECK(px < a_bp && i - e0 < kSB);
       const uint32_t old = atomicExch(&sm.head[px], tag | (uint32_t)(i - e0));
       sm.next[i - e0] = (old & 0xffff0000u) == tag ? (uint16_t)old : (uint16_t)kEmpty;
     }
@@ -151,6 +152,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
     if (cb + lane >= nch) break;
     const uint32_t me = wl[cb + lane];
     const int px = (int)(sub[e0 + me].y & 0x7fffffffu);
+    ESI_DCHECK(me < (uint32_t)(e1 - e0) && px < a_bp);
     uint32_t id[kSlots];
     id[0] = me;
     int c = 1;
@@ -161,7 +163,9 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
       c += (n != kEmpty) ? 1 : 0;
     }
     if (c == kSlots && sm.next[id[kSlots - 1]] != kEmpty) {   // > kSlots events: dense path
-      sm.dq[atomicAdd(sm.nd, 1u)] = (uint16_t)px;
+      const uint32_t slot = atomicAdd(sm.nd, 1u);
+      ESI_DCHECK(slot < (uint32_t)(kSB / 4));
+      sm.dq[slot] = (uint16_t)px;
       continue;
     }
     // claim order -> arrival order (kEmpty = 0xffff sorts after every index)
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kNT, 2) esi_integrate_kernel(IntArgs a) {
           __syncthreads();
           gen = 1;
         }
-        process_segment<BM>(sm, sub, e0, e1, trel32, gen, warp, lane, kc);
+        process_segment<BM>(sm, sub, e0, e1, trel32, gen, warp, lane, kc, npx);
       }
       if (e1 == n_sb) break;                    // the window may continue in the next sub-batch
       if (j >= f_hi) { done = true; break; }    // later events stay pending

@@ -194,6 +194,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     if (FULL || warp * WEV + r * 32 + lane < ne) {
       const uint32_t band = rk[r] >> 22;
       const uint32_t pos = boff[band] + hist[warp * nbp + band] + ((rk[r] >> 13) & 0x1ffu);
+      ESI_DCHECK(band < (uint32_t)a.nb && pos < (uint32_t)ne);
       sbuf[pos] = make_uint2(tl[r], (rk[r] & 0xfffu) | ((rk[r] & 0x1000u) << 19));
     }
   }
