@@ -30,8 +30,9 @@ namespace {
 
 constexpr int kNW = 16;                       // warps per CTA
 constexpr int kNT = kNW * 32;                 // threads per CTA
-constexpr int kEPT = 4;                       // events per thread per segment
+constexpr int kEPT = 6;                       // events per thread per segment
 constexpr int kSB = kNT * kEPT;               // events per sub-batch
+constexpr int kStage = (kEPT * 32 + 1) / 2;   // uint2 per warp: kEPT * 32 chain heads (u32)
 
 // Shared memory of one CTA, carved at run time (the band size is a run-time
 // multiple of 64 pixels chosen to balance the grid over the SMs).
@@ -41,7 +42,7 @@ struct FastSmem {
   uint32_t* head;                             // [bp] last claimer | generation << 16
   uint16_t* next;                             // [kSB] previous claimer (claim-order chain)
   uint2* sub[2];                              // [kSB] gathered sub-batches (double buffer), arrival order
-  uint2* stage;                               // [kNW][64] per-warp scratch: chain heads / dense compaction
+  uint2* stage;                               // [kNW][kStage] per-warp scratch: chain heads / dense compaction
   uint16_t* dq;                               // [kSB / 4] dense pixels of the segment
   uint32_t* nd;
   uint32_t* pre;                              // [n_tiles + 1]
@@ -50,7 +51,7 @@ struct FastSmem {
 
 __host__ __device__ inline size_t fast_smem_bytes(int bp, int n_tiles) {
   const size_t b = (size_t)bp;
-  return b * 12 + kSB * 2 + 2 * kSB * 8 + kNW * 64 * 8 + (kSB / 4) * 2 + 16 + (size_t)(2 * n_tiles + 1) * 4 + 64;
+  return b * 12 + kSB * 2 + 2 * kSB * 8 + kNW * kStage * 8 + (kSB / 4) * 2 + 16 + (size_t)(2 * n_tiles + 1) * 4 + 64;
 }
 
 __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_tiles) {
@@ -58,7 +59,7 @@ __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_til
   unsigned char* q = base;
   m.sub[0] = reinterpret_cast<uint2*>(q); q += kSB * 8;
   m.sub[1] = reinterpret_cast<uint2*>(q); q += kSB * 8;
-  m.stage = reinterpret_cast<uint2*>(q); q += kNW * 64 * 8;
+  m.stage = reinterpret_cast<uint2*>(q); q += kNW * kStage * 8;
   m.S = reinterpret_cast<float*>(q); q += (size_t)bp * 4;
   m.T = reinterpret_cast<float*>(q); q += (size_t)bp * 4;
   m.head = reinterpret_cast<uint32_t*>(q); q += (size_t)bp * 4;
@@ -128,7 +129,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
     }
   }
   __syncthreads();
-  uint32_t* wl = reinterpret_cast<uint32_t*>(sm.stage + warp * 64);   // <= kEPT * 32 chain heads
+  uint32_t* wl = reinterpret_cast<uint32_t*>(sm.stage + warp * kStage);   // <= kEPT * 32 chain heads
   int nch = 0;
 #pragma unroll
   for (int r = 0; r < kEPT; ++r) {                        // apply: singles now, chains deferred
@@ -196,7 +197,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
   const uint32_t nd = *sm.nd;
   if (nd > 0) {
     for (uint32_t d = warp; d < nd; d += kNW)
-      dense_pixel_apply<BM>(sm.S, sm.T, sub, sm.stage + warp * 64, e0, e1, sm.dq[d], trel, lane, k);
+      dense_pixel_apply<BM>(sm.S, sm.T, sub, sm.stage + warp * kStage, e0, e1, sm.dq[d], trel, lane, k);
     __syncthreads();
     if (tid == 0) *sm.nd = 0;
   }
