@@ -88,9 +88,14 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
 /* Appends n events (the Alg. 2 input E) to the handle's pending stream.
  * Events must be globally non-decreasing in t (reading A15) and later than the
  * last rendered frame.
- *  - host pointer: the events are copied to device memory (pinned-host sources
- *    are copied asynchronously on the handle's stream; pageable ones
- *    synchronously).  The caller may reuse the buffer when the call returns.
+ *  - pageable host pointer: the events are copied to device memory before the
+ *    call returns; the caller may reuse the buffer at once.
+ *  - pinned (page-locked) host pointer, e.g. cudaHostAlloc / torch pin_memory:
+ *    BORROWED.  esi_render* copies it to the device chunk by chunk on a copy
+ *    stream, overlapped with the kernels, so the caller must keep it alive and
+ *    unmodified until the render that integrates its last event has returned
+ *    (or until esi_reset/esi_destroy).  (With params.validate_on_push the batch
+ *    is copied at push time instead.)
  *  - device pointer: ZERO-COPY.  The library BORROWS the buffer: it reads it
  *    during later esi_render* calls (stream-ordered on the handle's stream), so
  *    the caller must keep it alive and unmodified until the render that
@@ -101,7 +106,9 @@ int esi_push_events(esi_handle_t* h, const esi_event_t* events, size_t n);
 /* Renders one frame at t_frame_us: integrates every pending event with
  * t <= t_frame_us (ties belong to the frame, reading A6), then writes the
  * width*height row-major 8-bit frame (index y*width + x) to out, which may be
- * a host or a device pointer.  Later events stay pending.  Synchronous. */
+ * a host or a device pointer (host: frames are copied back chunk by chunk,
+ * overlapped with the kernels; pinned host memory copies fastest).  Later
+ * events stay pending.  Synchronous. */
 int esi_render(esi_handle_t* h, int64_t t_frame_us, uint8_t* out);
 
 /* Renders n frames at the non-decreasing host array t_frames_us[0..n) into

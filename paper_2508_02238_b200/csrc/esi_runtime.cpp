@@ -25,16 +25,18 @@ using namespace esi;
 namespace {
 
 struct Segment {
-  const esi_event_t* ptr;  // first pending event
+  const esi_event_t* ptr;  // first pending event (device, or a device-accessible pinned host address)
   int64_t n;               // pending events
-  void* owned;             // device buffer owned by the handle (host pushes), or nullptr
+  void* owned;             // device buffer owned by the handle (pageable host pushes), or nullptr
   size_t owned_bytes;
+  bool host;               // borrowed pinned host buffer (copied to the device during render)
 };
 
 struct Chunk {
   const esi_event_t* ptr;
   int64_t n;
   int seg;
+  bool host;               // pinned host memory: staged to the device chunk by chunk during render
 };
 
 struct TimedLaunch {
@@ -64,6 +66,9 @@ struct esi_handle {
   int32_t* tile_wide[2] = {nullptr, nullptr};
   int64_t* wide_t[2] = {nullptr, nullptr};
   cudaStream_t aux = nullptr;               // K1 stream
+  cudaStream_t h2d = nullptr, d2h = nullptr; // copy streams of the pinned-host pipeline
+  esi_event_t* stage_ev[2] = {nullptr, nullptr};   // device staging of host chunks (double buffer)
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_d2h_done = nullptr;
   cudaEvent_t ev_k1[2] = {nullptr, nullptr}, ev_k2[2] = {nullptr, nullptr}, ev_start = nullptr;
   // small device buffers
   int64_t* d_tf = nullptr;
@@ -117,6 +122,21 @@ int cuda_fail(esi_handle_t* h, cudaError_t e) {
     cudaError_t e_ = (call);                       \
     if (e_ != cudaSuccess) return cuda_fail(h, e_); \
   } while (0)
+
+// 0: pageable host, 1: device / managed, 2: pinned (page-locked, device-accessible) host
+int ptr_kind(const void* p, const void** dev_alias) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return 1;
+  if (at.type == cudaMemoryTypeHost && at.devicePointer) {
+    if (dev_alias) *dev_alias = at.devicePointer;
+    return 2;
+  }
+  return 0;
+}
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes at;
@@ -428,6 +448,13 @@ void esi_destroy(esi_handle_t* h) {
   }
   if (h->ev_start) cudaEventDestroy(h->ev_start);
   if (h->aux) cudaStreamDestroy(h->aux);
+  for (int b = 0; b < 2; ++b) {
+    if (h->stage_ev[b]) cudaFree(h->stage_ev[b]);
+    if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
+  }
+  if (h->ev_d2h_done) cudaEventDestroy(h->ev_d2h_done);
+  if (h->h2d) { cudaStreamSynchronize(h->h2d); cudaStreamDestroy(h->h2d); }
+  if (h->d2h) { cudaStreamSynchronize(h->d2h); cudaStreamDestroy(h->d2h); }
   if (h->h_pin) cudaFreeHost(h->h_pin);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   cudaGetLastError();
@@ -470,8 +497,16 @@ int esi_push_events(esi_handle_t* h, const esi_event_t* events, size_t n) {
   if (n == 0) return ESI_OK;
   if (!events || ((uintptr_t)events & 7)) return ESI_ERR_INVALID_ARG;
   cudaSetDevice(h->prm.device);
-  Segment sg{events, (int64_t)n, nullptr, 0};
-  if (!is_device_ptr(events)) {
+  Segment sg{events, (int64_t)n, nullptr, 0, false};
+  const void* alias = nullptr;
+  const int kind = ptr_kind(events, &alias);
+  if (kind == 2 && !h->prm.validate_on_push) {
+    // pinned host buffer: borrowed; render copies it to the device chunk by chunk,
+    // overlapped with the kernels (the device reads it through its UVA alias only
+    // for a few boundary timestamps)
+    sg.ptr = (const esi_event_t*)alias;
+    sg.host = true;
+  } else if (kind != 1) {
     size_t got = 0;
     void* buf = pool_take(h, n * sizeof(esi_event_t), &got);
     if (!buf) return ESI_ERR_OOM;
@@ -549,7 +584,33 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
   std::vector<Chunk> chunks;
   for (int k = 0; k < (int)h->segs.size(); ++k)
     for (int64_t off = 0; off < h->segs[k].n; off += h->chunk_events)
-      chunks.push_back({h->segs[k].ptr + off, std::min(h->chunk_events, h->segs[k].n - off), k});
+      chunks.push_back({h->segs[k].ptr + off, std::min(h->chunk_events, h->segs[k].n - off), k, h->segs[k].host});
+  bool any_host = false;
+  for (const Chunk& ch : chunks) any_host |= ch.host;
+  if (any_host) {   // pinned-host pipeline: staging buffers + copy streams (created on first use)
+    for (int b = 0; b < 2 && !rc; ++b)
+      if (!h->stage_ev[b] && cudaMalloc((void**)&h->stage_ev[b], h->chunk_events * sizeof(esi_event_t)) != cudaSuccess) {
+        cudaGetLastError();
+        return ESI_ERR_OOM;
+      }
+    if (!h->h2d) {
+      if (cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_h2d[0], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_h2d[1], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_d2h_done, cudaEventDisableTiming) != cudaSuccess)
+        return cuda_fail(h, cudaGetLastError());
+    }
+  }
+  const bool stream_frames = !out_dev && !chunks.empty();   // frames copied back chunk by chunk
+  if (stream_frames && !h->d2h) {
+    if (cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_h2d[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_h2d[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_d2h_done, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_fail(h, cudaGetLastError());
+  }
 
   if (chunks.empty()) {
     ReadoutArgs ra{h->dS, h->dT, h->d_tf, (int32_t)F, dout, h->P, vec8, h->dp, h->mp};
@@ -599,8 +660,16 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       if (two && c >= 2) ESI_CUDA(h, cudaStreamWaitEvent(h->aux, h->ev_k2[bf], 0));
       const Chunk& ch = chunks[c];
       const int n_tiles = (int)((ch.n + kTile - 1) / kTile);
+      const esi_event_t* k1_ev = ch.ptr;
+      if (ch.host) {   // stage the chunk: H2D on the copy stream once K1(c-2) released the buffer
+        if (c >= 2) ESI_CUDA(h, cudaStreamWaitEvent(h->h2d, h->ev_k1[bf], 0));
+        ESI_CUDA(h, cudaMemcpyAsync(h->stage_ev[bf], ch.ptr, ch.n * sizeof(esi_event_t), cudaMemcpyDefault, h->h2d));
+        ESI_CUDA(h, cudaEventRecord(h->ev_h2d[bf], h->h2d));
+        ESI_CUDA(h, cudaStreamWaitEvent(k1s, h->ev_h2d[bf], 0));
+        k1_ev = h->stage_ev[bf];
+      }
       PartArgs pa;
-      pa.ev = ch.ptr;
+      pa.ev = k1_ev;
       pa.n = ch.n;
       pa.index_base = index_base;
       pa.prev_t = (c == 0) ? h->d_last_t : &chunks[c - 1].ptr[chunks[c - 1].n - 1].t_us;
@@ -623,10 +692,8 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       timed_begin(h, 0, &t1, k1s);
       ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, k1s));
       timed_end(h, &t1);
-      if (two) {
-        ESI_CUDA(h, cudaEventRecord(h->ev_k1[bf], h->aux));
-        ESI_CUDA(h, cudaStreamWaitEvent(st, h->ev_k1[bf], 0));
-      }
+      if (two || any_host) ESI_CUDA(h, cudaEventRecord(h->ev_k1[bf], k1s));
+      if (two) ESI_CUDA(h, cudaStreamWaitEvent(st, h->ev_k1[bf], 0));
 
       IntArgs ia;
       ia.info = h->d_info + c;
@@ -658,7 +725,13 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
         ESI_CUDA(h, launch_integrate(ia, st));
       }
       timed_end(h, &t2);
-      if (two) ESI_CUDA(h, cudaEventRecord(h->ev_k2[bf], st));
+      if (two || stream_frames) ESI_CUDA(h, cudaEventRecord(h->ev_k2[bf], st));
+      if (stream_frames && hinfo[c].f_hi > hinfo[c].f_lo) {   // this chunk's frames are final: copy them back
+        ESI_CUDA(h, cudaStreamWaitEvent(h->d2h, h->ev_k2[bf], 0));
+        const size_t o = (size_t)hinfo[c].f_lo * (size_t)h->P;
+        const size_t nbytes = (size_t)(hinfo[c].f_hi - hinfo[c].f_lo) * (size_t)h->P;
+        ESI_CUDA(h, cudaMemcpyAsync(out + o, dout + o, nbytes, cudaMemcpyDeviceToHost, h->d2h));
+      }
       h->st_launches += 2;
       h->st_chunks += 1;
       index_base += ch.n;
@@ -692,7 +765,8 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     }
     h->segs.swap(keep);
   }
-  if (!out_dev) ESI_CUDA(h, cudaMemcpyAsync(out, dout, frame_bytes, cudaMemcpyDeviceToHost, st));
+  if (!out_dev && chunks.empty()) ESI_CUDA(h, cudaMemcpyAsync(out, dout, frame_bytes, cudaMemcpyDeviceToHost, st));
+  if (stream_frames) ESI_CUDA(h, cudaStreamSynchronize(h->d2h));
   ESI_CUDA(h, cudaStreamSynchronize(st));
   collect_timing(h);
   h->has_last_frame = true;

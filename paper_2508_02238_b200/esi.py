@@ -194,8 +194,8 @@ class Esi:
 
     def push(self, events) -> int:
         rc = push_events(self.h, events)
-        if rc == ESI_OK and hasattr(events, "is_cuda") and events.is_cuda:
-            self._borrowed.append(events)
+        if rc == ESI_OK and hasattr(events, "is_cuda") and (events.is_cuda or events.is_pinned()):
+            self._borrowed.append(events)      # device and pinned host buffers are borrowed (esi.h)
         return rc
 
     def render(self, t_frame_us: int, out=None):

@@ -394,3 +394,43 @@ def test_c3_full_length_hot_pixels_dense_path():
     one frame window (chain and dense paths)."""
     w = wl("c3")
     check(w.W, w.H, ev_np_of(w), w.t_frames, w.params)
+
+
+def test_pinned_host_pipeline_equals_device_path():
+    """Pinned host events are borrowed and staged chunk by chunk during render
+    (copy stream overlapped with the kernels); host outputs are copied back per
+    chunk.  Same chunks, same kernels -> bit-identical to the device path."""
+    from paper_2508_02238_b200 import Esi
+    w = wl("c2", duration_us=500_000)
+    F = len(w.t_frames[w.t_frames <= 500_000])
+    tf = w.t_frames[:F]
+    res = {}
+    for mode in ("device", "pinned", "pinned_pageable_out"):
+        e = Esi(w.W, w.H, chunk_events=65536, **w.params)
+        try:
+            ev = w.events.cuda() if mode == "device" else w.events.pin_memory()
+            assert e.push(ev) == 0
+            if mode == "device":
+                out = torch.empty((F, w.H, w.W), dtype=torch.uint8, device="cuda")
+                e.render_many(tf[:F // 2], out[:F // 2])
+                e.render_many(tf[F // 2:], out[F // 2:])
+                frames = out.cpu().numpy()
+            elif mode == "pinned":
+                out = torch.empty((F, w.H, w.W), dtype=torch.uint8).pin_memory()
+                e.render_many(tf[:F // 2], out[:F // 2])
+                e.render_many(tf[F // 2:], out[F // 2:])
+                frames = out.numpy()
+            else:
+                frames = np.concatenate([e.render_many(tf[:F // 2]), e.render_many(tf[F // 2:])])
+            S, T = e.get_state()
+            res[mode] = (frames, S, T, e.last_render_stats())
+        finally:
+            e.close()
+    f0, S0, T0, st0 = res["device"]
+    assert st0["chunks"] >= 2
+    for mode in ("pinned", "pinned_pageable_out"):
+        f, S, T, _ = res[mode]
+        assert np.array_equal(f, f0), mode
+        assert np.array_equal(S, S0) and np.array_equal(T, T0), mode
+    ref, S_ref, T_ref = oracle_run(w.W, w.H, ev_np_of(w)[to_numpy_struct(w.events)["t"] <= tf[-1]], tf, w.params)
+    assert_frames_close(f0, ref)
