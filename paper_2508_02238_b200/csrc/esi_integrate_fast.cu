@@ -1,9 +1,9 @@
 // esi_integrate_fast.cu -- K2: per-band integration (Alg. 2) fused
 // with the Eq. 13/14 readout of every frame of the chunk.
 //
-// One CTA of 16 warps per band of band_px consecutive pixel ids (K1's
+// One CTA of 8 warps per band of band_px consecutive pixel ids (K1's
 // partition key; band_px is a run-time multiple of 64 chosen so that the grid
-// fills the SMs evenly).  The band's state lives in shared memory for the whole
+// is exactly three resident CTAs per SM).  The band's state lives in shared memory for the whole
 // chunk: S (fp32) and T as an fp32 offset from the chunk base ChunkInfo::trel
 // (exact integers: |T| < 2^24 us; pixels older than the decay horizon are
 // clamped to -(dt_cut+1), i.e. "fully decayed").
@@ -28,7 +28,7 @@ namespace {
 
 #include "esi_fast_common.cuh"
 
-constexpr int kNW = 16;                       // warps per CTA
+constexpr int kNW = 8;                        // warps per CTA
 constexpr int kNT = kNW * 32;                 // threads per CTA
 constexpr int kEPT = 6;                       // events per thread per segment
 constexpr int kSB = kNT * kEPT;               // events per sub-batch
@@ -239,7 +239,7 @@ __device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const 
 }
 
 template <int BM>
-__global__ void __launch_bounds__(kNT, 2) esi_integrate_kernel(IntArgs a) {
+__global__ void __launch_bounds__(kNT, 3) esi_integrate_kernel(IntArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_wsum[32];
   const int band = blockIdx.x;

@@ -345,13 +345,13 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   h->prm = prm;
   derive_params(h);
   // Band size (K1 partition key, K2 CTA): a multiple of 64 pixels such that
-  // the bands fill the SMs evenly at 2 resident K2 CTAs (16 warps each) per SM
-  // (c4: 294 bands of 3136 pixels on 148 SMs), at most kMaxBandPx (shared memory) and at most
+  // the bands fill the SMs evenly at 3 resident K2 CTAs (8 warps each) per SM
+  // (c4: 437 bands of 2112 pixels on 148 SMs), at most kMaxBandPx (shared memory) and at most
   // kMaxBands bands (K1's shared-memory histograms).
   {
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, prm.device);
-    const int64_t slots = (int64_t)n_sm * 2;
+    const int64_t slots = (int64_t)n_sm * 3;
     int64_t bp = (P + slots - 1) / slots;
     bp = ((bp + 63) / 64) * 64;
     bp = std::max<int64_t>(64, std::min<int64_t>(bp, kMaxBandPx));
