@@ -61,13 +61,6 @@ __device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
   if (tid == 0) v[n] = wsum[32 + kPartWarps - 1];
 }
 
-// Per-event register state between the ranking and the scatter (32 bits, plus
-// the low 32 bits of t): pixel-in-band (12) | sign of p (1) | warp-local rank
-// within the band (9, < 512 events per warp) | band (10, nb <= 1024).
-__device__ __forceinline__ uint32_t pack_rk(uint32_t pix, bool neg, uint32_t rank, uint32_t band) {
-  return pix | (neg ? 0x1000u : 0u) | (rank << 13) | (band << 22);
-}
-
 // RANK_ATOMIC: per-warp rank from a shared-memory atomicAdd on the warp's private
 // (u16-packed) histogram -- relies on same-address lanes being served in lane
 // order, which esi_probe_atomic_order checks at esi_create; otherwise ranks come
@@ -111,7 +104,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   __syncthreads();
 
   uint16_t* myhist = hist + warp * nbp;
-  uint32_t rk[EPT], tl[EPT];
+  uint32_t key[EPT], tl[EPT], pr[EPT];   // band | rank << 10; record words (t low, pixel | sign)
   const uint32_t W = (uint32_t)a.W, H = (uint32_t)a.H, BPX = (uint32_t)a.band_px;
   const int64_t t_min = a.t_min;
   const int64_t tprev0 = s_tprev;
@@ -166,7 +159,8 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
       rank = base + rl;
     }
     tl[r] = (uint32_t)t;
-    rk[r] = pack_rk(pix, p < 0 && !(act && bad), rank, band);
+    pr[r] = pix | ((p < 0 && !(act && bad)) ? 0x80000000u : 0u);
+    key[r] = band | (rank << 10);
   }
   __syncthreads();                               // raw consumed: its first half becomes sbuf
 
@@ -192,10 +186,10 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     if (FULL || warp * WEV + r * 32 + lane < ne) {
-      const uint32_t band = rk[r] >> 22;
-      const uint32_t pos = boff[band] + hist[warp * nbp + band] + ((rk[r] >> 13) & 0x1ffu);
+      const uint32_t band = key[r] & 0x3ffu;
+      const uint32_t pos = boff[band] + hist[warp * nbp + band] + (key[r] >> 10);
       ESI_DCHECK(band < (uint32_t)a.nb && pos < (uint32_t)ne);
-      sbuf[pos] = make_uint2(tl[r], (rk[r] & 0xfffu) | ((rk[r] & 0x1000u) << 19));
+      sbuf[pos] = make_uint2(tl[r], pr[r]);
     }
   }
   if (threadIdx.x == 0) {
@@ -224,8 +218,8 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     for (int r = 0; r < EPT; ++r) {
       const int i = warp * WEV + r * 32 + lane;
       if (i < ne) {
-        const uint32_t band = rk[r] >> 22;
-        const uint32_t pos = boff[band] + hist[warp * nbp + band] + ((rk[r] >> 13) & 0x1ffu);
+        const uint32_t band = key[r] & 0x3ffu;
+        const uint32_t pos = boff[band] + hist[warp * nbp + band] + (key[r] >> 10);
         a.wide_t[e0 + pos] = ev[i].t_us;
       }
     }
@@ -234,7 +228,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
 }
 
 template <bool RANK_ATOMIC>
-__global__ void __launch_bounds__(kPartThreads, 3) esi_partition_kernel(PartArgs a) {
+__global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   // Chunk entirely after the last frame of this render: nothing to integrate.
   if (a.ev[0].t_us > a.t_cap) return;
