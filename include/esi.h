@@ -70,7 +70,7 @@ typedef struct {
                             0: Alg. 2 literal, frame maps the stored S             */
   int32_t device;        /* CUDA device ordinal                                            */
   int32_t validate_on_push; /* 1: eager, atomic validation in esi_push_events (see above) */
-  int32_t chunk_events;  /* events per pipeline chunk; 0 = default (4 Mi)                  */
+  int32_t chunk_events;  /* events per pipeline chunk; 0 = default (8 Mi)                  */
 } esi_params_t;
 
 typedef struct esi_handle esi_handle_t;

@@ -209,14 +209,12 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
 __device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const uint32_t* pre, const uint32_t* mt,
                                            int n_tiles, int n_b, int sb0, uint2* dst, int warp, int lane) {
   const uint32_t q_end = (uint32_t)min(sb0 + kSB, n_b);
-  int t_lo;                                     // last tile with pre[t] <= sb0 (32-ary search)
-  {
-    const int c = lane * 32;
-    const unsigned b1 = __ballot_sync(kFull, c < n_tiles && pre[c] <= (uint32_t)sb0);
-    const int blk = 31 - __clz(b1 | 1u);
-    const int t = blk * 32 + lane;
-    const unsigned b2 = __ballot_sync(kFull, t < n_tiles && pre[t] <= (uint32_t)sb0);
-    t_lo = blk * 32 + (31 - __clz(b2 | 1u));
+  int t_lo = 0;                                 // last tile with pre[t] <= sb0 (32-ary search)
+#pragma unroll
+  for (int stride = 1024; stride >= 1; stride >>= 5) {
+    const int t = t_lo + lane * stride;
+    const unsigned b = __ballot_sync(kFull, t < n_tiles && pre[t] <= (uint32_t)sb0);
+    t_lo += (31 - __clz(b | 1u)) * stride;
   }
   for (int tb = t_lo + warp * 8; tb < n_tiles; tb += kNW * 8) {
     if (pre[tb] >= q_end) break;                // segments are in order: the rest is later

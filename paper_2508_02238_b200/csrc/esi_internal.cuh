@@ -22,7 +22,7 @@ constexpr int kTile = 4096;          // events per partition tile
 constexpr int kPartThreads = 512;    // 16 warps x 8 events per thread
 constexpr int kPartWarps = kPartThreads / 32;
 constexpr int kSubBatch = 1024;      // band events staged in smem per sub-batch
-constexpr int kMaxTilesPerChunk = 1024;
+constexpr int kMaxTilesPerChunk = 2048;
 constexpr int kWarpPx = 256;         // pixels owned by one warp (8 per lane)
 constexpr int kMaxBands = 1024;
 constexpr int kMaxBandPx = 4096;

@@ -364,7 +364,7 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   }
   h->nb = (int)((P + h->band_px - 1) / h->band_px);
   h->band_magic = ((uint64_t)1 << 40) / (uint64_t)h->band_px + 1;   // exact pid / band_px for pid < 2^23
-  int64_t ce = prm.chunk_events > 0 ? prm.chunk_events : (int64_t)4 << 20;
+  int64_t ce = prm.chunk_events > 0 ? prm.chunk_events : (int64_t)8 << 20;
   ce = ((ce + kTile - 1) / kTile) * kTile;
   ce = std::min<int64_t>(ce, (int64_t)kMaxTilesPerChunk * kTile);
   h->chunk_events = ce;
