@@ -33,6 +33,7 @@ constexpr int kNT = kNW * 32;                 // threads per CTA
 constexpr int kEPT = 6;                       // events per thread per segment
 constexpr int kSB = kNT * kEPT;               // events per sub-batch
 constexpr int kStage = (kEPT * 32 + 1) / 2;   // uint2 per warp: kEPT * 32 chain heads (u32)
+constexpr int kWinCap = 32;                   // window ends listed per pass (warp 0, per sub-batch)
 
 // Shared memory of one CTA, carved at run time (the band size is a run-time
 // multiple of 64 pixels chosen to balance the grid over the SMs).
@@ -45,13 +46,15 @@ struct FastSmem {
   uint2* stage;                               // [kNW][kStage] per-warp scratch: chain heads / dense compaction
   uint16_t* dq;                               // [kSB / 4] dense pixels of the segment
   uint32_t* nd;
+  int32_t* wend;                              // [kWinCap] window ends inside the current sub-batch
   uint32_t* pre;                              // [n_tiles + 1]
   uint32_t* mt;                               // [n_tiles]
 };
 
 __host__ __device__ inline size_t fast_smem_bytes(int bp, int n_tiles) {
   const size_t b = (size_t)bp;
-  return b * 12 + kSB * 2 + 2 * kSB * 8 + kNW * kStage * 8 + (kSB / 4) * 2 + 16 + (size_t)(2 * n_tiles + 1) * 4 + 64;
+  return b * 12 + kSB * 2 + 2 * kSB * 8 + kNW * kStage * 8 + (kSB / 4) * 2 + 16 + kWinCap * 4 +
+         (size_t)(2 * n_tiles + 1) * 4 + 64;
 }
 
 __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_tiles) {
@@ -66,6 +69,7 @@ __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_til
   m.pre = reinterpret_cast<uint32_t*>(q); q += (size_t)(n_tiles + 1) * 4;
   m.mt = reinterpret_cast<uint32_t*>(q); q += (size_t)n_tiles * 4;
   m.nd = reinterpret_cast<uint32_t*>(q); q += 16;
+  m.wend = reinterpret_cast<int32_t*>(q); q += kWinCap * 4;
   m.next = reinterpret_cast<uint16_t*>(q); q += kSB * 2;
   m.dq = reinterpret_cast<uint16_t*>(q);
   return m;
@@ -76,9 +80,8 @@ __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_til
 // Frame j for the band: 4 pixels per thread-iteration (quads), Eq. 4 + Eq. 13 +
 // Eq. 14 with packed f32x2 arithmetic, one 4-byte streaming store per quad.
 template <int BM>
-__device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm, int j, int64_t trel,
+__device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm, int j, int32_t tji,
                                              int64_t px0, int npx, const FastConst& c) {
-  const int32_t tji = (int32_t)(a.tf[j] - trel);
   const float tj = (float)tji;
   const float aj = (float)(tji - (int32_t)c.tau_h);          // t_j - tau (folded mode: tau integer)
   uint8_t* frame = a.out + (int64_t)j * a.P + px0;
@@ -309,31 +312,54 @@ __global__ void __launch_bounds__(kNT, 3) esi_integrate_kernel(IntArgs a) {
     cp_async_wait_all();
     __syncthreads();
     if (sb0 + kSB < n_b) gather_sub(a.rec, sm.pre, sm.mt, n_tiles, n_b, sb0 + kSB, (kb & 1) ? sm.sub[0] : sm.sub[1], warp, lane);
-    // ---- 2. segments = frame windows inside the sub-batch; readout at each window end
+    // ---- 2. segments = frame windows inside the sub-batch; readout at each window end.
+    // Window ends (events of the sub-batch with t <= t_j) are listed by warp 0,
+    // kWinCap at a time, behind one barrier, instead of being searched by every warp.
     int e0 = 0;
-    while (true) {
-      const int e1 = e0 + upper_bound_rel<kSB>(sub + e0, n_sb - e0, trel32, tj, lane);   // same in every warp
-      if (e1 > e0) {
-        if (++gen == 0xffffu) {                 // generation tags exhausted: clear the claim table
-          __syncthreads();
-          for (int i = threadIdx.x; i < bp; i += kNT) sm.head[i] = 0u;
-          __syncthreads();
-          gen = 1;
+    bool more = true;
+    while (more) {
+      more = false;
+      if (warp == 0) {
+        int e = e0, w = 0, jj = j;
+        int32_t tw = tj;
+        while (true) {
+          e += upper_bound_rel<kSB>(sub + e, n_sb - e, trel32, tw, lane);
+          if (lane == 0) sm.wend[w] = e;
+          ++w;
+          if (e == n_sb || jj >= f_hi || w == kWinCap - 1) break;
+          ++jj;
+          tw = (jj < f_hi) ? (int32_t)(a.tf[jj] - trel) : tcap;
         }
-        process_segment<BM>(sm, sub, e0, e1, trel32, gen, warp, lane, kc, npx);
+        if (lane == 0) sm.wend[kWinCap - 1] = w;   // count in the last slot (at most kWinCap - 1 windows)
       }
-      if (e1 == n_sb) break;                    // the window may continue in the next sub-batch
-      if (j >= f_hi) { done = true; break; }    // later events stay pending
-      fast_readout<BM>(a, sm, j, trel, px0, npx, kc);
-      ++j;
-      tj = (j < f_hi) ? (int32_t)(a.tf[j] - trel) : tcap;
-      e0 = e1;
+      __syncthreads();
+      const int nwin = sm.wend[kWinCap - 1];
+      for (int w = 0; w < nwin; ++w) {
+        const int e1 = sm.wend[w];
+        if (e1 > e0) {
+          if (++gen == 0xffffu) {               // generation tags exhausted: clear the claim table
+            __syncthreads();
+            for (int i = threadIdx.x; i < bp; i += kNT) sm.head[i] = 0u;
+            __syncthreads();
+            gen = 1;
+          }
+          process_segment<BM>(sm, sub, e0, e1, trel32, gen, warp, lane, kc, npx);
+        }
+        if (e1 == n_sb) break;                  // the window may continue in the next sub-batch
+        if (j >= f_hi) { done = true; break; }  // later events stay pending
+        fast_readout<BM>(a, sm, j, tj, px0, npx, kc);
+        ++j;
+        tj = (j < f_hi) ? (int32_t)(a.tf[j] - trel) : tcap;
+        e0 = e1;
+        more = (w == nwin - 1);                 // every listed window closed: list the next ones
+      }
+      if (more) __syncthreads();                // wend is rewritten by warp 0
     }
   }
   cp_async_wait_all();
   // ---- 3. frames after the chunk's last event
   while (j < f_hi) {
-    fast_readout<BM>(a, sm, j, trel, px0, npx, kc);
+    fast_readout<BM>(a, sm, j, (int32_t)(a.tf[j] - trel), px0, npx, kc);
     ++j;
   }
   if (n_b > 0) {
