@@ -39,57 +39,58 @@ __global__ void __launch_bounds__(kRouteThreads) esi_route_hist_kernel(const esi
   const int64_t e0 = (int64_t)blockIdx.x * kRouteTile;
   const int ne = (int)min((int64_t)kRouteTile, n - e0);
   const int4* evv = reinterpret_cast<const int4*>(ev + e0);
-  for (int i = threadIdx.x; i < ne; i += kRouteThreads) {
-    const int4 r = __ldg(evv + i);
-    const uint32_t y = (uint32_t)r.z >> 16;
-    if (y >= (uint32_t)H) {
-      atomicMin(err, ((unsigned long long)(e0 + i) << 8) | (unsigned)ESI_ERR_OUT_OF_BOUNDS);
-      continue;
+  for (int ib = 0; ib < ne; ib += kRouteThreads) {     // warp-aggregated counts (few bands: avoid
+    const int i = ib + threadIdx.x;                     // same-address shared atomics per event)
+    int b = -1;
+    if (i < ne) {
+      const int4 r = __ldg(evv + i);
+      const uint32_t y = (uint32_t)r.z >> 16;
+      if (y >= (uint32_t)H) atomicMin(err, ((unsigned long long)(e0 + i) << 8) | (unsigned)ESI_ERR_OUT_OF_BOUNDS);
+      else b = route_band_of(y, rr.start, nb);
     }
-    atomicAdd(&cnt[route_band_of(y, rr.start, nb)], 1u);
+    const unsigned peers = __match_any_sync(kFull, b);
+    if (b >= 0 && (peers & lanemask_lt()) == 0u) atomicAdd(&cnt[b], (uint32_t)__popc(peers));
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += kRouteThreads) tile_cnt[(int64_t)b * gridDim.x + blockIdx.x] = cnt[b];
 }
 
 // One CTA per band: exclusive prefix over the band's tile counts, in place; total -> band_tot[b].
+// Each thread sums a contiguous run of tiles, one block scan combines the runs.
 __global__ void __launch_bounds__(1024) esi_route_scan_kernel(uint32_t* tile_cnt, int n_tiles,
                                                               int64_t* band_tot) {
   __shared__ uint32_t wsum[32];
-  __shared__ uint64_t s_carry;
   const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* c = tile_cnt + (int64_t)b * n_tiles;
-  if (threadIdx.x == 0) s_carry = 0;
+  const int per = (n_tiles + 1023) / 1024;
+  const int t0 = threadIdx.x * per, t1 = min(n_tiles, t0 + per);
+  uint32_t local = 0;
+  for (int t = t0; t < t1; ++t) local += c[t];
+  uint32_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
   __syncthreads();
-  for (int t0 = 0; t0 < n_tiles; t0 += 1024) {
-    const int t = t0 + threadIdx.x;
-    const uint32_t v = t < n_tiles ? c[t] : 0u;
-    uint32_t x = v;
+  if (warp == 0) {
+    uint32_t w = wsum[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, x, o);
-      if (lane >= o) x += y;
+      const uint32_t y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
     }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t w = wsum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, w, o);
-        if (lane >= o) w += y;
-      }
-      wsum[lane] = w;   // inclusive
-    }
-    __syncthreads();
-    const uint64_t carry = s_carry;
-    const uint32_t excl = x - v + (warp ? wsum[warp - 1] : 0u);
-    if (t < n_tiles) c[t] = (uint32_t)(carry + excl);   // band-local offsets fit 32 bits (n < 2^32)
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry = carry + wsum[31];
-    __syncthreads();
+    wsum[lane] = w;   // inclusive
   }
-  if (threadIdx.x == 0) band_tot[b] = (int64_t)s_carry;
+  __syncthreads();
+  uint32_t run = x - local + (warp ? wsum[warp - 1] : 0u);   // band-local offsets fit 32 bits (n < 2^32)
+  for (int t = t0; t < t1; ++t) {
+    const uint32_t v = c[t];
+    c[t] = run;
+    run += v;
+  }
+  if (threadIdx.x == 1023) band_tot[b] = (int64_t)run;
 }
 
 __global__ void __launch_bounds__(kRouteThreads) esi_route_scatter_kernel(const esi_event_t* ev, int64_t n,
