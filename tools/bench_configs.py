@@ -21,7 +21,8 @@ from paper_2508_02238_b200 import Esi  # noqa: E402
 
 def run(name, fps=100):
     t0 = time.time()
-    w = make_workload(name, "cuda", fps=fps) if name == "c4" else make_workload(name, "cuda")
+    w = make_workload(name, "cuda", fps=fps) if name == "c4" else make_workload(name, "cpu")
+    w.events = w.events.cuda()
     gen_s = time.time() - t0
     tf = w.t_frames if name == "c4" else frame_times(w.duration_us, fps)
     F = len(tf)
