@@ -1,14 +1,16 @@
 // esi_internal.cuh -- device-side types and launchers of libesi (sm_100a).
 //
 // Pipeline of one render call:
-//   plan      : which chunks hold events with t <= last frame time        (tiny)
-//   per chunk of <= chunk_events pending events:
-//     K1 esi_partition_kernel : 16-B vector ingest + validation + stable,
-//        bit-exact partition of each 8192-event tile by pixel band
-//     K2 esi_integrate_kernel : one CTA per band; gathers the band's events
-//        in arrival order, applies Alg. 2 per event (per-pixel arrival order
-//        kept by lowest-lane-first rounds) to the band's state in shared
-//        memory, and writes every frame of the chunk (fused Eq. 14 readout)
+//   plan      : per chunk: time base, frames it renders, fast-path eligibility (tiny)
+//   per chunk of <= chunk_events pending events (K1 of chunk c+1 on a
+//   low-priority aux stream overlaps K2 of chunk c; double-buffered scratch):
+//     K1 esi_partition_kernel : 16-B ingest (cp.async-staged 4096-event tiles) +
+//        validation + stable, bit-exact partition of each tile by pixel band
+//     K2 esi_integrate_kernel : one CTA per band (esi_integrate_fast.cu; fp64
+//        fallback esi_integrate.cu); gathers the band's events in arrival order,
+//        applies Alg. 2 per frame window (claim chains: sparse / chain / dense
+//        warp-scan paths) to the band's state in shared memory, and writes every
+//        frame of the chunk (fused Eq. 13/14 readout)
 //   consume   : how many pending events were integrated                   (tiny)
 //   K4 esi_readout_kernel   : frames when no event is pending (readout only)
 #pragma once
