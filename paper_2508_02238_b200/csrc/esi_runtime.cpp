@@ -835,6 +835,14 @@ int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t
   if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_INVALID_ARG; }
   if (!is_device_ptr(events) || !is_device_ptr(out)) return ESI_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
+  {   // keep the stream-ordered scratch mapped between calls (the default pool would unmap it at every sync)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   RouteRows rr;
   for (int b = 0; b <= 64; ++b) rr.start[b] = b <= n_bands ? row_start[b] : height;
   const int64_t n_tiles = route_tiles((int64_t)n);
