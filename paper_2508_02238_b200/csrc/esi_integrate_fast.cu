@@ -86,6 +86,32 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
   const float aj = (float)(tji - (int32_t)c.tau_h);          // t_j - tau (folded mode: tau integer)
   uint8_t* frame = a.out + (int64_t)j * a.P + px0;
   const int nq = (npx + 3) >> 2;
+  const bool vec = a.vec8 != 0;
+  if (c.fold) {                                              // hot path: constants hoisted out of the loop
+    const float2 naj = make_float2(-aj, -aj);
+    const float2 sw2 = make_float2(c.scale_w2, c.scale_w2), off = make_float2(c.off_frac, c.off_frac);
+    const float2 mo = make_float2(c.magic_off, c.magic_off);
+    const float4* S4 = reinterpret_cast<const float4*>(sm.S);
+    const float4* T4 = reinterpret_cast<const float4*>(sm.T);
+    for (int q = threadIdx.x; q < nq; q += kNT) {
+      const float4 s0 = S4[q], t0 = T4[q];
+      float2 w0 = __fadd2_rn(make_float2(t0.x, t0.y), naj), w1 = __fadd2_rn(make_float2(t0.z, t0.w), naj);
+      w0.x = fmaxf(w0.x, 0.f); w0.y = fmaxf(w0.y, 0.f); w1.x = fmaxf(w1.x, 0.f); w1.y = fmaxf(w1.y, 0.f);
+      const float2 v0 = __fmul2_rn(make_float2(s0.x, s0.y), __fmul2_rn(w0, w0));
+      const float2 v1 = __fmul2_rn(make_float2(s0.z, s0.w), __fmul2_rn(w1, w1));
+      const float2 r0 = __fadd2_rd(__ffma2_rn(v0, sw2, off), mo), r1 = __fadd2_rd(__ffma2_rn(v1, sw2, off), mo);
+      const uint32_t v = __byte_perm(__byte_perm(__float_as_uint(r0.x), __float_as_uint(r0.y), 0x0040),
+                                     __byte_perm(__float_as_uint(r1.x), __float_as_uint(r1.y), 0x0040), 0x5410);
+      const int base = q * 4;
+      if (vec && base + 4 <= npx) {
+        st_stream4(frame + base, v);
+      } else {
+        const int n = min(4, npx - base);
+        for (int u = 0; u < n; ++u) frame[base + u] = (uint8_t)((v >> (8 * u)) & 0xffu);
+      }
+    }
+    return;
+  }
   for (int q = threadIdx.x; q < nq; q += kNT) {
     const int base = q * 4;
     const float4 s0 = *reinterpret_cast<const float4*>(&sm.S[base]);
@@ -93,7 +119,7 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
     const uint32_t b01 = readout2<BM>(make_float2(s0.x, s0.y), make_float2(t0.x, t0.y), tj, aj, c);
     const uint32_t b23 = readout2<BM>(make_float2(s0.z, s0.w), make_float2(t0.z, t0.w), tj, aj, c);
     const uint32_t v = __byte_perm(b01, b23, 0x5410);
-    if (a.vec8 && base + 4 <= npx) {
+    if (vec && base + 4 <= npx) {
       st_stream4(frame + base, v);
     } else {
       const int n = min(4, npx - base);
