@@ -154,6 +154,48 @@ int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t
                     const int32_t* row_start, int32_t n_bands, esi_event_t* out, int64_t* counts,
                     void* stream);
 
+/* Two-phase router for the multi-GPU exchange over peer memory.  The all-to-all
+ * of the row-band split is done by the router's own scatter kernel: each
+ * source rank writes its band-b run straight into band b's receive buffer on
+ * the GPU that owns band b (NVLink P2P stores through a CUDA IPC mapping), so
+ * the exchange overlaps the partition arithmetic tile by tile and needs no
+ * staging copy.
+ *   esi_router_create   row bands as for esi_route_bands (1 <= n_bands <= 64).
+ *   esi_router_count    counts (HOST, n_bands) = events of the DEVICE array
+ *                       `events` per band; synchronises `stream`.  The events
+ *                       must stay valid and unchanged until the scatter has run.
+ *                       y >= height: ESI_ERR_OUT_OF_BOUNDS.
+ *   esi_router_scatter  writes band b's events, in arrival order and with y
+ *                       rebased, to dst[b] + dst_offset[b] (records; dst is a
+ *                       HOST array of n_bands DEVICE pointers, 16-byte aligned,
+ *                       local or peer-mapped, each with room for
+ *                       dst_offset[b] + counts[b] records).  Stream-ordered on
+ *                       `stream`, no synchronisation: the caller makes the
+ *                       destination's reader wait (stream sync + a host
+ *                       barrier across the ranks).
+ * The router owns its scratch (grown on demand) and frees it in
+ * esi_router_destroy. */
+typedef struct esi_router esi_router_t;
+int esi_router_create(int32_t device, int32_t height, const int32_t* row_start, int32_t n_bands,
+                      esi_router_t** out);
+int esi_router_count(esi_router_t* r, const esi_event_t* events, size_t n, int64_t* counts, void* stream);
+int esi_router_scatter(esi_router_t* r, esi_event_t* const* dst, const int64_t* dst_offset, void* stream);
+void esi_router_destroy(esi_router_t* r);
+
+/* Receive buffers shared between processes: plain cudaMalloc allocations
+ * (esi_buffer_alloc / esi_buffer_free, owned by the allocating process),
+ * exported with esi_ipc_get_handle (ESI_IPC_HANDLE_BYTES opaque bytes, sent to
+ * the peers by the caller) and mapped by a peer with esi_ipc_open (peer access
+ * enabled lazily) until esi_ipc_close.  A process cannot open its own handle:
+ * it uses its own pointer.  esi_stream_sync: cudaStreamSynchronize. */
+#define ESI_IPC_HANDLE_BYTES 64
+int esi_buffer_alloc(int32_t device, size_t bytes, void** ptr);
+int esi_buffer_free(int32_t device, void* ptr);
+int esi_ipc_get_handle(const void* ptr, void* handle);
+int esi_ipc_open(int32_t device, const void* handle, void** ptr);
+int esi_ipc_close(int32_t device, void* ptr);
+int esi_stream_sync(int32_t device, void* stream);
+
 /* ---- instrumentation (used by bench.py and the parity tests) -------------- */
 
 /* Per-kernel device time accumulated by the handle when timing is enabled

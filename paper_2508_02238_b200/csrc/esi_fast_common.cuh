@@ -7,7 +7,6 @@
 constexpr int kSlots = 8;   // events of one pixel in one segment applied by a single thread
 constexpr uint32_t kEmpty = 0xffffu;
 
-constexpr float kMagic = 8388608.0f;   // 2^23
 
 struct FastConst {
   float tau_h, tau_l;                  // tau = 1e6/k us = tau_h + tau_l
@@ -34,7 +33,7 @@ __device__ __forceinline__ FastConst make_const(const IntArgs& a) {
   c.smax = a.mp.smax;
   c.scale = a.mp.scale;
   c.off_frac = a.mp.off_frac;
-  c.magic_off = kMagic + (float)a.mp.off_int;
+  c.magic_off = a.mp.magic_off;
   c.scale_w2 = a.mp.scale_w2;
   c.tau_int = a.dp.tau_l == 0.f;
   c.rd = a.mp.readout_decay != 0;

@@ -3,7 +3,7 @@
 //
 // One CTA of 8 warps per band of band_px consecutive pixel ids (K1's
 // partition key; band_px is a run-time multiple of 64 chosen so that the grid
-// is exactly three resident CTAs per SM).  The band's state lives in shared memory for the whole
+// is exactly kK2Ctas resident CTAs per SM).  The band's state lives in shared memory for the whole
 // chunk: S (fp32) and T as an fp32 offset from the chunk base ChunkInfo::trel
 // (exact integers: |T| < 2^24 us; pixels older than the decay horizon are
 // clamped to -(dt_cut+1), i.e. "fully decayed").
@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kNW = 8;                        // warps per CTA
 constexpr int kNT = kNW * 32;                 // threads per CTA
-constexpr int kEPT = 6;                       // events per thread per segment
+constexpr int kEPT = kK2Ctas >= 4 ? 4 : 6;    // events per thread per segment (smem budget)
 constexpr int kSB = kNT * kEPT;               // events per sub-batch
 constexpr int kStage = (kEPT * 32 + 1) / 2;   // uint2 per warp: kEPT * 32 chain heads (u32)
 constexpr int kWinCap = 32;                   // window ends listed per pass (warp 0, per sub-batch)
@@ -47,14 +47,14 @@ struct FastSmem {
   uint16_t* dq;                               // [kSB / 4] dense pixels of the segment
   uint32_t* nd;
   int32_t* wend;                              // [kWinCap] window ends inside the current sub-batch
-  uint32_t* pre;                              // [n_tiles + 1]
-  uint32_t* mt;                               // [n_tiles]
+  uint32_t* pre;                              // [n_tiles + 1] band events before tile t
+  uint16_t* mo;                               // [n_tiles] offset of the band's run inside tile t
 };
 
 __host__ __device__ inline size_t fast_smem_bytes(int bp, int n_tiles) {
   const size_t b = (size_t)bp;
   return b * 12 + kSB * 2 + 2 * kSB * 8 + kNW * kStage * 8 + (kSB / 4) * 2 + 16 + kWinCap * 4 +
-         (size_t)(2 * n_tiles + 1) * 4 + 64;
+         (size_t)(n_tiles + 1) * 4 + (((size_t)n_tiles * 2 + 15) & ~(size_t)15) + 64;
 }
 
 __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_tiles) {
@@ -67,7 +67,7 @@ __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_til
   m.T = reinterpret_cast<float*>(q); q += (size_t)bp * 4;
   m.head = reinterpret_cast<uint32_t*>(q); q += (size_t)bp * 4;
   m.pre = reinterpret_cast<uint32_t*>(q); q += (size_t)(n_tiles + 1) * 4;
-  m.mt = reinterpret_cast<uint32_t*>(q); q += (size_t)n_tiles * 4;
+  m.mo = reinterpret_cast<uint16_t*>(q); q += ((size_t)n_tiles * 2 + 15) & ~(size_t)15;
   m.nd = reinterpret_cast<uint32_t*>(q); q += 16;
   m.wend = reinterpret_cast<int32_t*>(q); q += kWinCap * 4;
   m.next = reinterpret_cast<uint16_t*>(q); q += kSB * 2;
@@ -235,7 +235,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
 
 // Gather band events [sb0, min(sb0 + kSB, n_b)) into dst with cp.async: 8 (tile,
 // band) segments per warp step, 4 lanes per segment, tiles in order = arrival order.
-__device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const uint32_t* pre, const uint32_t* mt,
+__device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const uint32_t* pre, const uint16_t* mo,
                                            int n_tiles, int n_b, int sb0, uint2* dst, int warp, int lane) {
   const uint32_t q_end = (uint32_t)min(sb0 + kSB, n_b);
   int t_lo = 0;                                 // last tile with pre[t] <= sb0 (32-ary search)
@@ -252,12 +252,11 @@ __device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const 
     const uint2* src = rec;
     if (t < n_tiles) {
       p0 = pre[t];
-      const uint32_t m = mt[t];
       if (p0 < q_end) {
         i0 = p0 < (uint32_t)sb0 ? (uint32_t)sb0 - p0 : 0u;
-        i1 = min(m >> 16, q_end - p0);
+        i1 = min(pre[t + 1], q_end) - p0;
       }
-      src += (size_t)t * kTile + (m & 0xffffu);
+      src += (size_t)t * kTile + mo[t];
     }
     const int dofs = (int)p0 - sb0;             // >= -i0
     for (uint32_t i = i0 + (lane & 3); i < i1; i += 4) cp_async8(&dst[dofs + (int)i], src + i);
@@ -266,7 +265,7 @@ __device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const 
 }
 
 template <int BM>
-__global__ void __launch_bounds__(kNT, 3) esi_integrate_kernel(IntArgs a) {
+__global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_wsum[32];
   const int band = blockIdx.x;
@@ -296,12 +295,15 @@ __global__ void __launch_bounds__(kNT, 3) esi_integrate_kernel(IntArgs a) {
   if (threadIdx.x == 0) *sm.nd = 0;
   int n_b = 0;
   if (active) {
-    for (int t = threadIdx.x; t < n_tiles; t += kNT) sm.mt[t] = a.meta[(int64_t)band * n_tiles + t];
-    __syncthreads();
+    const uint32_t* meta = a.meta + (int64_t)band * n_tiles;
     const int per = (n_tiles + kNT - 1) / kNT;
     const int t0 = threadIdx.x * per;
     uint32_t local = 0;
-    for (int t = t0; t < min(n_tiles, t0 + per); ++t) local += sm.mt[t] >> 16;
+    for (int t = t0; t < min(n_tiles, t0 + per); ++t) {
+      const uint32_t m = meta[t];
+      sm.mo[t] = (uint16_t)(m & 0xffffu);
+      local += m >> 16;
+    }
     uint32_t x = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(kNT, 3) esi_integrate_kernel(IntArgs a) {
     }
     for (int t = t0; t < min(n_tiles, t0 + per); ++t) {
       sm.pre[t] = run;
-      run += sm.mt[t] >> 16;
+      run += meta[t] >> 16;
     }
     if (threadIdx.x == 0) sm.pre[n_tiles] = tot;
     n_b = (int)tot;
@@ -331,13 +333,13 @@ __global__ void __launch_bounds__(kNT, 3) esi_integrate_kernel(IntArgs a) {
   bool done = false;
   uint32_t gen = 0;
   // ---- 1. gather sub-batch k into sub[k & 1]; sub-batch k+1 is in flight while k is integrated
-  if (n_b > 0) gather_sub(a.rec, sm.pre, sm.mt, n_tiles, n_b, 0, sm.sub[0], warp, lane);
+  if (n_b > 0) gather_sub(a.rec, sm.pre, sm.mo, n_tiles, n_b, 0, sm.sub[0], warp, lane);
   for (int sb0 = 0, kb = 0; sb0 < n_b && !done; sb0 += kSB, ++kb) {
     const int n_sb = min(kSB, n_b - sb0);
     const uint2* sub = (kb & 1) ? sm.sub[1] : sm.sub[0];   // no dynamic index into sm (keeps it in registers)
     cp_async_wait_all();
     __syncthreads();
-    if (sb0 + kSB < n_b) gather_sub(a.rec, sm.pre, sm.mt, n_tiles, n_b, sb0 + kSB, (kb & 1) ? sm.sub[0] : sm.sub[1], warp, lane);
+    if (sb0 + kSB < n_b) gather_sub(a.rec, sm.pre, sm.mo, n_tiles, n_b, sb0 + kSB, (kb & 1) ? sm.sub[0] : sm.sub[1], warp, lane);
     // ---- 2. segments = frame windows inside the sub-batch; readout at each window end.
     // Window ends (events of the sub-batch with t <= t_j) are listed by warp 0,
     // kWinCap at a time, behind one barrier, instead of being searched by every warp.

@@ -28,6 +28,12 @@ constexpr int kMaxTilesPerChunk = 2048;
 constexpr int kWarpPx = 256;         // pixels owned by one warp (8 per lane)
 constexpr int kMaxBands = 1024;
 constexpr int kMaxBandPx = 4096;
+// Resident fast-K2 CTAs (8 warps each) per SM that the band size targets; the
+// kernel's events per thread per sub-batch follow from the shared-memory budget.
+#ifndef ESI_K2_CTAS
+#define ESI_K2_CTAS 3
+#endif
+constexpr int kK2Ctas = ESI_K2_CTAS;
 
 // First error of a render call: (global event index << 8) | code, atomicMin'ed
 // so that the earliest offending event wins (same as the oracle's first error).
@@ -52,6 +58,7 @@ struct MapParams {
   float scale, off_frac;
   float scale_w2;        // (k * 1e-6)^2 * scale: folded b = 2 readout of the fast K2
   int32_t off_int;
+  float magic_off;       // 2^23 + off_int (exact): RD-add magic of the fast K2 readout
   int32_t readout_decay;
 };
 
@@ -153,9 +160,15 @@ cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s);
 cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,
                            int64_t* last_t, cudaStream_t s);
 // row-band routing (esi_route.cu): hist + scan + stable scatter on stream s
-cudaError_t launch_route(const esi_event_t* ev, int64_t n, int32_t H, int nb, const RouteRows& rr,
-                         uint32_t* tile_cnt, int64_t* band_tot, esi_event_t* out,
-                         unsigned long long* err, cudaStream_t s);
+struct RouteDst {
+  esi_event_t* ptr[64];      // per band: destination buffer (local or a peer GPU's)
+  int64_t off[64];           // per band: first record of this source's run in ptr[b]
+};
+cudaError_t launch_route_count(const esi_event_t* ev, int64_t n, int32_t H, int nb, const RouteRows& rr,
+                               uint32_t* tile_cnt, int64_t* band_tot, unsigned long long* err, cudaStream_t s);
+cudaError_t launch_route_scatter(const esi_event_t* ev, int64_t n, int32_t H, int nb, const RouteRows& rr,
+                                 const uint32_t* tile_off, const int64_t* band_tot, const RouteDst& dst,
+                                 cudaStream_t s);
 int64_t route_tiles(int64_t n);
 cudaError_t launch_fill_i64(int64_t* p, int64_t n, int64_t v, cudaStream_t s);
 cudaError_t launch_validate(const esi_event_t* ev, int64_t n, const int64_t* prev_t,

@@ -14,7 +14,10 @@
 //   1. histogram: one CTA per 4096-event tile, per-tile band counts
 //   2. scan:      one CTA per band, exclusive prefix of its tile counts + total
 //   3. scatter:   one CTA per tile, stable in-tile ranks (warp ballot multi-split
-//                 over the band bits + per-warp counts), 16-B record writes
+//                 over the band bits + per-warp counts), 16-B record writes to a
+//                 per-band destination pointer, which may live on a peer GPU
+//                 (esi_router_scatter: the all-to-all exchange is done by the
+//                 scatter's own NVLink stores, overlapped tile by tile)
 #include "esi_device.cuh"
 
 namespace esi {
@@ -93,13 +96,18 @@ __global__ void __launch_bounds__(1024) esi_route_scan_kernel(uint32_t* tile_cnt
   if (threadIdx.x == 1023) band_tot[b] = (int64_t)run;
 }
 
+// Scatter: band b's run of this tile goes to dst.ptr[b] + dst.off[b] + (events of
+// band b in earlier tiles) + in-tile rank.  dst.ptr[b] may be a peer GPU's
+// buffer (NVLink P2P stores): the exchange of esi_router_scatter is this kernel.
+// With band_tot != nullptr (esi_route_bands), every band goes to one buffer at
+// the exclusive prefix of the band totals.
 __global__ void __launch_bounds__(kRouteThreads) esi_route_scatter_kernel(const esi_event_t* ev, int64_t n,
                                                                           int32_t H, int nb, RouteRows rr,
                                                                           const uint32_t* tile_off,
                                                                           const int64_t* band_tot,
-                                                                          esi_event_t* out) {
+                                                                          RouteDst dst) {
   __shared__ uint32_t wcnt[kRouteThreads / 32][kRouteMaxBands];
-  __shared__ int64_t base[kRouteMaxBands];
+  __shared__ int4* base[kRouteMaxBands];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
   const int64_t e0 = (int64_t)tile * kRouteTile;
@@ -109,8 +117,9 @@ __global__ void __launch_bounds__(kRouteThreads) esi_route_scatter_kernel(const 
   if (threadIdx.x == 0) {
     int64_t run = 0;
     for (int b = 0; b < nb; ++b) {
-      base[b] = run + tile_off[(int64_t)b * gridDim.x + tile];
-      run += band_tot[b];
+      const int64_t off = band_tot ? run : dst.off[b];
+      base[b] = reinterpret_cast<int4*>(dst.ptr[b]) + off + tile_off[(int64_t)b * gridDim.x + tile];
+      if (band_tot) run += band_tot[b];
     }
   }
   __syncthreads();
@@ -159,18 +168,23 @@ __global__ void __launch_bounds__(kRouteThreads) esi_route_scatter_kernel(const 
   for (int r = 0; r < kPer; ++r) {
     if (rk[r] == 0xffffffffu) continue;
     const int b = (int)(rk[r] >> 16);
-    const int64_t pos = base[b] + wcnt[warp][b] + (rk[r] & 0xffffu);
-    reinterpret_cast<int4*>(out)[pos] = rec[r];
+    base[b][wcnt[warp][b] + (rk[r] & 0xffffu)] = rec[r];
   }
 }
 
-cudaError_t launch_route(const esi_event_t* ev, int64_t n, int32_t H, int nb, const RouteRows& rr,
-                         uint32_t* tile_cnt, int64_t* band_tot, esi_event_t* out,
-                         unsigned long long* err, cudaStream_t s) {
+cudaError_t launch_route_count(const esi_event_t* ev, int64_t n, int32_t H, int nb, const RouteRows& rr,
+                               uint32_t* tile_cnt, int64_t* band_tot, unsigned long long* err, cudaStream_t s) {
   const int n_tiles = (int)((n + kRouteTile - 1) / kRouteTile);
   esi_route_hist_kernel<<<n_tiles, kRouteThreads, 0, s>>>(ev, n, H, nb, rr, tile_cnt, err);
   esi_route_scan_kernel<<<nb, 1024, 0, s>>>(tile_cnt, n_tiles, band_tot);
-  esi_route_scatter_kernel<<<n_tiles, kRouteThreads, 0, s>>>(ev, n, H, nb, rr, tile_cnt, band_tot, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route_scatter(const esi_event_t* ev, int64_t n, int32_t H, int nb, const RouteRows& rr,
+                                 const uint32_t* tile_off, const int64_t* band_tot, const RouteDst& dst,
+                                 cudaStream_t s) {
+  const int n_tiles = (int)((n + kRouteTile - 1) / kRouteTile);
+  esi_route_scatter_kernel<<<n_tiles, kRouteThreads, 0, s>>>(ev, n, H, nb, rr, tile_off, band_tot, dst);
   return cudaGetLastError();
 }
 

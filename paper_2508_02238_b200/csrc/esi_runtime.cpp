@@ -277,6 +277,7 @@ void derive_params(esi_handle_t* h) {
   const double off = -p.s_min * 255.0 / range + 0.5;
   h->mp.off_int = (int32_t)std::floor(off);
   h->mp.off_frac = (float)(off - std::floor(off));
+  h->mp.magic_off = (float)(8388608.0 + (double)h->mp.off_int);
   h->mp.readout_decay = p.readout_decay ? 1 : 0;
   h->wp.C = p.C;
   h->wp.k_us = kk;
@@ -345,13 +346,13 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   h->prm = prm;
   derive_params(h);
   // Band size (K1 partition key, K2 CTA): a multiple of 64 pixels such that
-  // the bands fill the SMs evenly at 3 resident K2 CTAs (8 warps each) per SM
-  // (c4: 437 bands of 2112 pixels on 148 SMs), at most kMaxBandPx (shared memory) and at most
+  // the bands fill the SMs evenly at kK2Ctas resident K2 CTAs (8 warps each) per SM
+  // (c4, 4 per SM: 576 bands of 1600 pixels on 148 SMs), at most kMaxBandPx (shared memory) and at most
   // kMaxBands bands (K1's shared-memory histograms).
   {
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, prm.device);
-    const int64_t slots = (int64_t)n_sm * 3;
+    const int64_t slots = (int64_t)n_sm * kK2Ctas;
     int64_t bp = (P + slots - 1) / slots;
     bp = ((bp + 63) / 64) * 64;
     bp = std::max<int64_t>(64, std::min<int64_t>(bp, kMaxBandPx));
@@ -819,13 +820,121 @@ int esi_last_render_stats(esi_handle_t* h, int64_t* launches, int64_t* events, i
   return ESI_OK;
 }
 
-int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t height,
-                    const int32_t* row_start, int32_t n_bands, esi_event_t* out, int64_t* counts,
-                    void* stream) {
-  if (!row_start || !counts || n_bands < 1 || n_bands > 64 || height < 1) return ESI_ERR_INVALID_ARG;
+// ---- row-band router ------------------------------------------------------
+struct esi_router {
+  int32_t device = 0, height = 0, nb = 0;
+  RouteRows rr;
+  unsigned char* scratch = nullptr;   // band_tot[64] | err | tile_cnt[nb][n_tiles]
+  size_t cap = 0;
+  const esi_event_t* ev = nullptr;    // the counted events (caller-owned)
+  int64_t n = 0;
+  bool counted = false;
+};
+
+static int router_check_rows(int32_t height, const int32_t* row_start, int32_t n_bands) {
+  if (!row_start || n_bands < 1 || n_bands > 64 || height < 1) return ESI_ERR_INVALID_ARG;
   if (row_start[0] != 0 || row_start[n_bands] != height) return ESI_ERR_INVALID_ARG;
   for (int b = 0; b < n_bands; ++b)
     if (row_start[b + 1] <= row_start[b]) return ESI_ERR_INVALID_ARG;
+  return ESI_OK;
+}
+
+int esi_router_create(int32_t device, int32_t height, const int32_t* row_start, int32_t n_bands,
+                      esi_router_t** out) {
+  if (!out) return ESI_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (int rc = router_check_rows(height, row_start, n_bands)) return rc;
+  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_INVALID_ARG; }
+  esi_router_t* r = new esi_router_t();
+  r->device = device;
+  r->height = height;
+  r->nb = n_bands;
+  for (int b = 0; b <= 64; ++b) r->rr.start[b] = b <= n_bands ? row_start[b] : height;
+  *out = r;
+  return ESI_OK;
+}
+
+int esi_router_count(esi_router_t* r, const esi_event_t* events, size_t n, int64_t* counts, void* stream) {
+  if (!r || !counts) return ESI_ERR_INVALID_ARG;
+  r->counted = false;
+  if (n == 0) {
+    for (int b = 0; b < r->nb; ++b) counts[b] = 0;
+    r->ev = nullptr;
+    r->n = 0;
+    r->counted = true;
+    return ESI_OK;
+  }
+  if (!events || ((uintptr_t)events & 15) || n >= ((size_t)1 << 32)) return ESI_ERR_INVALID_ARG;
+  if (cudaSetDevice(r->device) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_INVALID_ARG; }
+  if (!is_device_ptr(events)) return ESI_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n_tiles = route_tiles((int64_t)n);
+  const size_t need = 64 * sizeof(int64_t) + 16 + (size_t)r->nb * n_tiles * sizeof(uint32_t);
+  if (need > r->cap) {
+    const size_t cap = std::max(need, r->cap * 2);
+    if (r->scratch && (cudaStreamSynchronize(st) != cudaSuccess || cudaFree(r->scratch) != cudaSuccess)) {
+      cudaGetLastError();
+      return ESI_ERR_CUDA;
+    }
+    r->scratch = nullptr;
+    r->cap = 0;
+    if (cudaMalloc((void**)&r->scratch, cap) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_OOM; }
+    r->cap = cap;
+  }
+  int64_t* band_tot = (int64_t*)r->scratch;
+  unsigned long long* err = (unsigned long long*)(r->scratch + 64 * sizeof(int64_t));
+  uint32_t* tile_cnt = (uint32_t*)(r->scratch + 64 * sizeof(int64_t) + 16);
+  unsigned long long herr = kNoError;
+  if (cudaMemsetAsync(err, 0xff, sizeof(*err), st) != cudaSuccess ||
+      launch_route_count(events, (int64_t)n, r->height, r->nb, r->rr, tile_cnt, band_tot, err, st) != cudaSuccess ||
+      cudaMemcpyAsync(counts, band_tot, r->nb * sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&herr, err, sizeof(herr), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    if (getenv("ESI_DEBUG")) fprintf(stderr, "[esi] route count: %s\n", cudaGetErrorString(cudaGetLastError()));
+    cudaGetLastError();
+    return ESI_ERR_CUDA;
+  }
+  if (herr != kNoError) return (int)(herr & 0xff);
+  r->ev = events;
+  r->n = (int64_t)n;
+  r->counted = true;
+  return ESI_OK;
+}
+
+int esi_router_scatter(esi_router_t* r, esi_event_t* const* dst, const int64_t* dst_offset, void* stream) {
+  if (!r || !dst || !dst_offset || !r->counted) return ESI_ERR_INVALID_ARG;
+  if (r->n == 0) return ESI_OK;
+  RouteDst d;
+  for (int b = 0; b < 64; ++b) {
+    d.ptr[b] = b < r->nb ? dst[b] : nullptr;
+    d.off[b] = b < r->nb ? dst_offset[b] : 0;
+    if (b < r->nb && (!dst[b] || ((uintptr_t)dst[b] & 15) || dst_offset[b] < 0)) return ESI_ERR_INVALID_ARG;
+  }
+  if (cudaSetDevice(r->device) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_INVALID_ARG; }
+  const uint32_t* tile_off = (const uint32_t*)(r->scratch + 64 * sizeof(int64_t) + 16);
+  if (launch_route_scatter(r->ev, r->n, r->height, r->nb, r->rr, tile_off, nullptr, d, (cudaStream_t)stream) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return ESI_ERR_CUDA;
+  }
+  return ESI_OK;
+}
+
+void esi_router_destroy(esi_router_t* r) {
+  if (!r) return;
+  if (r->scratch) {
+    cudaSetDevice(r->device);
+    cudaDeviceSynchronize();
+    cudaFree(r->scratch);
+  }
+  delete r;
+}
+
+int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t height,
+                    const int32_t* row_start, int32_t n_bands, esi_event_t* out, int64_t* counts,
+                    void* stream) {
+  if (!counts) return ESI_ERR_INVALID_ARG;
+  if (int rc = router_check_rows(height, row_start, n_bands)) return rc;
   if (n == 0) {
     for (int b = 0; b < n_bands; ++b) counts[b] = 0;
     return ESI_OK;
@@ -845,20 +954,23 @@ int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t
   }
   RouteRows rr;
   for (int b = 0; b <= 64; ++b) rr.start[b] = b <= n_bands ? row_start[b] : height;
+  RouteDst d;
+  for (int b = 0; b < 64; ++b) {
+    d.ptr[b] = out;
+    d.off[b] = 0;
+  }
   const int64_t n_tiles = route_tiles((int64_t)n);
-  uint32_t* tile_cnt = nullptr;
-  int64_t* band_tot = nullptr;
-  unsigned long long* err = nullptr;
   const size_t bytes = (size_t)n_bands * n_tiles * sizeof(uint32_t) + 64 * sizeof(int64_t) + 16;
   unsigned char* scratch = nullptr;
   if (cudaMallocAsync((void**)&scratch, bytes, st) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_OOM; }
-  band_tot = (int64_t*)scratch;
-  err = (unsigned long long*)(scratch + 64 * sizeof(int64_t));
-  tile_cnt = (uint32_t*)(scratch + 64 * sizeof(int64_t) + 16);
+  int64_t* band_tot = (int64_t*)scratch;
+  unsigned long long* err = (unsigned long long*)(scratch + 64 * sizeof(int64_t));
+  uint32_t* tile_cnt = (uint32_t*)(scratch + 64 * sizeof(int64_t) + 16);
   int rc = ESI_OK;
   unsigned long long herr = kNoError;
   if (cudaMemsetAsync(err, 0xff, sizeof(*err), st) != cudaSuccess ||
-      launch_route(events, (int64_t)n, height, n_bands, rr, tile_cnt, band_tot, out, err, st) != cudaSuccess ||
+      launch_route_count(events, (int64_t)n, height, n_bands, rr, tile_cnt, band_tot, err, st) != cudaSuccess ||
+      launch_route_scatter(events, (int64_t)n, height, n_bands, rr, tile_cnt, band_tot, d, st) != cudaSuccess ||
       cudaMemcpyAsync(counts, band_tot, n_bands * sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaMemcpyAsync(&herr, err, sizeof(herr), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaFreeAsync(scratch, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
@@ -868,6 +980,61 @@ int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t
   }
   if (herr != kNoError) rc = (int)(herr & 0xff);
   return rc;
+}
+
+// ---- device buffers shared between processes (CUDA IPC) for the P2P exchange
+int esi_buffer_alloc(int32_t device, size_t bytes, void** ptr) {
+  if (!ptr || bytes == 0) return ESI_ERR_INVALID_ARG;
+  *ptr = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_INVALID_ARG; }
+  if (cudaMalloc(ptr, bytes) != cudaSuccess) { cudaGetLastError(); *ptr = nullptr; return ESI_ERR_OOM; }
+  return ESI_OK;
+}
+
+int esi_buffer_free(int32_t device, void* ptr) {
+  if (!ptr) return ESI_OK;
+  if (cudaSetDevice(device) != cudaSuccess || cudaFree(ptr) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_CUDA; }
+  return ESI_OK;
+}
+
+int esi_ipc_get_handle(const void* ptr, void* handle) {
+  if (!ptr || !handle) return ESI_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t hd;
+  if (cudaIpcGetMemHandle(&hd, const_cast<void*>(ptr)) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_CUDA; }
+  static_assert(sizeof(hd) == ESI_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &hd, sizeof(hd));
+  return ESI_OK;
+}
+
+int esi_ipc_open(int32_t device, const void* handle, void** ptr) {
+  if (!handle || !ptr) return ESI_ERR_INVALID_ARG;
+  *ptr = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_INVALID_ARG; }
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof(hd));
+  if (cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    *ptr = nullptr;
+    return ESI_ERR_CUDA;
+  }
+  return ESI_OK;
+}
+
+int esi_ipc_close(int32_t device, void* ptr) {
+  if (!ptr) return ESI_OK;
+  if (cudaSetDevice(device) != cudaSuccess || cudaIpcCloseMemHandle(ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return ESI_ERR_CUDA;
+  }
+  return ESI_OK;
+}
+
+int esi_stream_sync(int32_t device, void* stream) {
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) {
+    cudaGetLastError();
+    return ESI_ERR_CUDA;
+  }
+  return ESI_OK;
 }
 
 int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8_t* out_p,

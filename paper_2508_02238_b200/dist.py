@@ -11,18 +11,25 @@ NCCL over NVLink on the GPU box, gloo in the CPU tests):
 * ``RowBandSharded`` -- one large sensor (config 5b) is split into G row bands
   (``row_bands``).  Each rank holds a time-contiguous shard of the raw stream
   (rank order = time order); it stably partitions the shard by band on its GPU
-  (``esi_route_bands``), exchanges the band buckets with one all-to-all, and
-  integrates its band's events -- received in source-rank order, i.e. time
-  order -- with an ordinary handle of height = band rows (y rebased by the
-  router).  Frames are assembled with all_gather_into_tensor: bands are
-  row-contiguous, so rank order is row-major order and every frame lands in
-  place.  The collectives only move bytes; all arithmetic runs in libesi's
-  kernels.
+  and the band buckets are exchanged so that every rank integrates its band's
+  events -- received in source-rank order, i.e. time order -- with an ordinary
+  handle of height = band rows (y rebased by the router).  Two exchanges:
+    - ``transport=PeerTransport(...)`` (the product path on NVLink): the
+      router's scatter kernel stores every event straight into the receive
+      arena of the rank that owns its band (CUDA IPC mapping, P2P stores), so
+      the all-to-all IS the partition kernel; only the per-band counts go
+      through a collective (a G x G all_gather) to place each source's run;
+    - otherwise ``esi_route_bands`` into a local buffer + NCCL
+      ``all_to_all_single`` (the baseline).
+  Frames are assembled with all_gather_into_tensor: bands are row-contiguous,
+  so rank order is row-major order and every frame lands in place.  All
+  arithmetic runs in libesi's kernels.
 
-The band handle and the router are injectable (``band_factory``, ``router``)
-so that the host logic -- routing plan, exchange, assembly -- is testable with
-world_size 2 on CPU (gloo) against a full-sensor reference; the product path
-uses libesi handles and the device router and has no CPU fallback.
+The band handle, the router and the transport are injectable (``band_factory``,
+``router``, ``transport``) so that the host logic -- routing plan, receive
+offsets, arena growth, exchange, assembly -- is testable with world_size 2 on
+CPU (gloo) against a full-sensor reference; the product path uses libesi
+handles and kernels and has no CPU fallback.
 """
 from __future__ import annotations
 
@@ -74,11 +81,93 @@ def device_router(device: int, height: int) -> Callable:
     return route
 
 
+class PeerTransport:
+    """P2P exchange of the row-band split on the GPUs (product path).
+
+    count(): esi_router_count of this rank's shard (per-band counts, host).
+    scatter(): esi_router_scatter -- band g's run is stored by the kernel
+    directly into dst[g] (rank g's receive arena, mapped into this process with
+    CUDA IPC; this rank's own arena by its pointer) at the given record offset.
+    Arenas are plain cudaMalloc buffers (esi_buffer_alloc) so that their IPC
+    handles cover them exactly."""
+
+    def __init__(self, device: int, height: int, starts: Sequence[int], stream: Optional[int] = None):
+        from .esi import _lib
+        self.L = _lib()
+        self.device = int(device)
+        self.G = len(starts) - 1
+        rs = (ctypes.c_int32 * (self.G + 1))(*starts)
+        r = ctypes.c_void_p()
+        self._check(self.L.esi_router_create(self.device, int(height), rs, self.G, ctypes.byref(r)), "router_create")
+        self.r = r
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        self._shard = None
+
+    @staticmethod
+    def _check(rc, what):
+        if rc != 0:
+            from .esi import EsiError
+            raise EsiError(rc, f"esi_{what}")
+
+    def count(self, shard: torch.Tensor) -> np.ndarray:
+        counts = np.zeros(self.G, np.int64)
+        n = int(shard.shape[0])
+        self._shard = shard                       # must stay valid until scatter
+        self._check(self.L.esi_router_count(self.r, shard.data_ptr() if n else None, n,
+                                            counts.ctypes.data, self.stream), "router_count")
+        return counts
+
+    def scatter(self, dst: Sequence[int], offsets: np.ndarray):
+        ptrs = (ctypes.c_void_p * self.G)(*[int(d) for d in dst])
+        off = np.ascontiguousarray(offsets, np.int64)
+        self._check(self.L.esi_router_scatter(self.r, ptrs, off.ctypes.data, self.stream), "router_scatter")
+
+    def sync(self):
+        self._check(self.L.esi_stream_sync(self.device, self.stream), "stream_sync")
+        self._shard = None
+
+    def alloc(self, nrec: int) -> int:
+        p = ctypes.c_void_p()
+        self._check(self.L.esi_buffer_alloc(self.device, int(nrec) * 16, ctypes.byref(p)), "buffer_alloc")
+        return int(p.value)
+
+    def free(self, addr: int):
+        self._check(self.L.esi_buffer_free(self.device, addr), "buffer_free")
+
+    def export(self, addr: int) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        self._check(self.L.esi_ipc_get_handle(addr, h), "ipc_get_handle")
+        return h.raw
+
+    def open(self, handle: bytes) -> int:
+        p = ctypes.c_void_p()
+        self._check(self.L.esi_ipc_open(self.device, handle, ctypes.byref(p)), "ipc_open")
+        return int(p.value)
+
+    def unmap(self, addr: int):
+        self._check(self.L.esi_ipc_close(self.device, addr), "ipc_close")
+
+    def push(self, band, addr: int, off: int, n: int) -> int:
+        return band.push_ptr(addr + 16 * int(off), int(n)) if n else 0
+
+    def quiesce(self):
+        """Every stream of the device idle (the band handle's renders included)."""
+        torch.cuda.synchronize(self.device)
+
+    def close(self):
+        if getattr(self, "r", None) is not None:
+            self.L.esi_router_destroy(self.r)
+            self.r = None
+
+
 class RowBandSharded:
     """One sensor split into row bands, one band per rank (see module docstring)."""
 
+    MIN_ARENA = 1 << 20                                     # records (16 MB) per receive arena
+
     def __init__(self, width: int, height: int, group=None, band_factory: Optional[Callable] = None,
-                 router: Optional[Callable] = None, device: Optional[torch.device] = None, **params):
+                 router: Optional[Callable] = None, device: Optional[torch.device] = None,
+                 transport=None, **params):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -92,15 +181,32 @@ class RowBandSharded:
             from .esi import Esi
             band_factory = lambda w, h, **p: Esi(w, h, **p)   # noqa: E731
         self.band = band_factory(self.W, self.rows, **params)
-        self.router = router if router is not None else device_router(self.device.index or 0, self.H)
+        self.p2p = transport
+        if transport is None:
+            self.router = router if router is not None else device_router(self.device.index or 0, self.H)
         self._keep = []
         self.stats = {"routed": 0, "sent": 0, "received": 0}
+        # P2P receive arenas: every rank tracks every arena's capacity and fill,
+        # which evolve deterministically from the all-gathered counts.
+        self._cap = [0] * self.world
+        self._fill = [0] * self.world
+        self._arena = None                                   # this rank's arena (transport id)
+        self._dst = [None] * self.world                      # where this rank writes band g
+        self._old = []                                       # replaced arenas, freed once consumed
 
     def close(self):
         if getattr(self, "band", None) is not None and hasattr(self.band, "close"):
             self.band.close()
         self.band = None
         self._keep = []
+        if self.p2p is not None:
+            for g, d in enumerate(self._dst):
+                if d is not None and g != self.rank:
+                    self.p2p.unmap(d)
+            for a in self._old + ([self._arena] if self._arena is not None else []):
+                self.p2p.free(a)
+            self._old, self._arena, self._dst = [], None, [None] * self.world
+            self.p2p.close()
 
     # -- routing + exchange -------------------------------------------------
     def exchange(self, shard: torch.Tensor) -> torch.Tensor:
@@ -124,9 +230,52 @@ class RowBandSharded:
         """Collective: every rank calls it once per round with its shard of the
         round's time slice; the concatenation of the shards in rank order must be
         time-ordered, and each round must follow the previous one in time."""
+        if self.p2p is not None:
+            return self._push_shard_p2p(shard)
         band_events = self.exchange(shard)
         self._keep.append(band_events)                      # device pushes are borrowed zero-copy
         return self.band.push(band_events)
+
+    def _push_shard_p2p(self, shard: torch.Tensor) -> int:
+        T, G, r = self.p2p, self.world, self.rank
+        counts = torch.as_tensor(np.asarray(T.count(shard), np.int64), device=self.device)
+        M = torch.empty((G, G), dtype=torch.int64, device=self.device)
+        dist.all_gather_into_tensor(M.view(-1), counts, group=self.group)
+        M = M.cpu().numpy()                                  # M[s, g]: events of source s for band g
+        R = M.sum(axis=0)                                    # this round's events per band
+        grow = [self._fill[g] + int(R[g]) > self._cap[g] for g in range(G)]
+        if any(grow):                                        # deterministic on every rank
+            for g in range(G):
+                if grow[g]:
+                    self._cap[g] = max(2 * self._cap[g], int(R[g]), self.MIN_ARENA)
+                    self._fill[g] = 0
+            if grow[r]:
+                if self._arena is not None:
+                    self._old.append(self._arena)            # may hold pending events: freed after render
+                self._arena = T.alloc(self._cap[r])
+            handles = [None] * G
+            dist.all_gather_object(handles, T.export(self._arena) if grow[r] else None, group=self.group)
+            for g in range(G):
+                if not grow[g]:
+                    continue
+                if g == r:
+                    self._dst[g] = self._arena
+                else:
+                    if self._dst[g] is not None:
+                        T.unmap(self._dst[g])
+                    self._dst[g] = T.open(handles[g])
+        off = np.array([self._fill[g] + int(M[:r, g].sum()) for g in range(G)], np.int64)
+        T.scatter(self._dst, off)                            # the exchange: P2P stores by the router kernel
+        T.sync()
+        dist.barrier(group=self.group)                       # every source's stores have landed
+        n_mine = int(R[r])
+        rc = T.push(self.band, self._arena, self._fill[r], n_mine)
+        for g in range(G):
+            self._fill[g] += int(R[g])
+        self.stats["routed"] += int(shard.shape[0])
+        self.stats["sent"] += int(M[r].sum() - M[r, r])
+        self.stats["received"] += n_mine
+        return rc
 
     # -- rendering + assembly -----------------------------------------------
     def render_many(self, t_frames, out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -147,6 +296,8 @@ class RowBandSharded:
         for j in range(F):                                   # frame j: rank-major = row-major
             dist.all_gather_into_tensor(buf[j].view(-1), band[j].view(-1), group=self.group)
         self._keep = []
+        if self.p2p is not None:
+            self._recycle_arenas()
         if direct:
             return out
         res = buf[:, :self.H]
@@ -154,6 +305,22 @@ class RowBandSharded:
             out.copy_(res)
             return out
         return res.contiguous()
+
+    def _recycle_arenas(self):
+        """After a render: arenas whose events are all integrated are reused from
+        the start (every rank must agree, so the decision is all-gathered)."""
+        (self.p2p.quiesce if hasattr(self.p2p, "quiesce") else self.p2p.sync)()
+        pending = int(self.band.pending()) if hasattr(self.band, "pending") else 1
+        flags = torch.tensor([1 if pending == 0 else 0], dtype=torch.int64, device=self.device)
+        allf = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        dist.all_gather_into_tensor(allf, flags, group=self.group)
+        for g, f in enumerate(allf.cpu().tolist()):
+            if f:
+                self._fill[g] = 0
+        if pending == 0:
+            for a in self._old:
+                self.p2p.free(a)
+            self._old = []
 
     def get_state(self):
         return self.band.get_state()

@@ -79,6 +79,21 @@ def _lib():
         L.esi_kernel_time.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.esi_last_render_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.esi_debug_partition.argtypes = [vp, vp, vp, vp, sz, vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+        L.esi_router_create.argtypes = [i32, i32, vp, i32, ctypes.POINTER(vp)]
+        L.esi_router_count.argtypes = [vp, vp, sz, vp, vp]
+        L.esi_router_scatter.argtypes = [vp, vp, vp, vp]
+        L.esi_router_destroy.argtypes = [vp]
+        L.esi_router_destroy.restype = None
+        L.esi_buffer_alloc.argtypes = [i32, sz, ctypes.POINTER(vp)]
+        L.esi_buffer_free.argtypes = [i32, vp]
+        L.esi_ipc_get_handle.argtypes = [vp, vp]
+        L.esi_ipc_open.argtypes = [i32, vp, ctypes.POINTER(vp)]
+        L.esi_ipc_close.argtypes = [i32, vp]
+        L.esi_stream_sync.argtypes = [i32, vp]
+        for f in ("esi_router_create", "esi_router_count", "esi_router_scatter", "esi_route_bands",
+                  "esi_buffer_alloc", "esi_buffer_free", "esi_ipc_get_handle", "esi_ipc_open",
+                  "esi_ipc_close", "esi_stream_sync"):
+            getattr(L, f).restype = ctypes.c_int
         for f in ("esi_create", "esi_push_events", "esi_render", "esi_render_many", "esi_get_state",
                   "esi_set_state", "esi_reset", "esi_set_stream", "esi_get_error",
                   "esi_enable_kernel_timing", "esi_kernel_time", "esi_last_render_stats",
@@ -182,7 +197,9 @@ class Esi:
         self.P = self.W * self.H
         self.params = default_params(**params)
         self.h = create(self.W, self.H, self.params)
-        self._borrowed = []          # keep borrowed device buffers alive
+        self._borrowed = []          # (buffer, cumulative end): borrowed buffers kept alive until consumed
+        self._pushed = 0             # events pushed since create/reset
+        self._consumed = 0           # events integrated by renders since create/reset
 
     def close(self):
         if getattr(self, "h", None):
@@ -194,14 +211,34 @@ class Esi:
 
     def push(self, events) -> int:
         rc = push_events(self.h, events)
-        if rc == ESI_OK and hasattr(events, "is_cuda") and (events.is_cuda or events.is_pinned()):
-            self._borrowed.append(events)      # device and pinned host buffers are borrowed (esi.h)
+        if rc == ESI_OK:
+            self._pushed += _nbytes(events) // 16
+            if hasattr(events, "is_cuda") and (events.is_cuda or events.is_pinned()):
+                self._borrowed.append((events, self._pushed))   # borrowed until integrated (esi.h)
         return rc
+
+    def push_ptr(self, ptr: int, n: int, keep=None) -> int:
+        """Pushes n events at a raw device (or pinned host) address, e.g. a P2P
+        receive buffer; `keep` is held until the events are integrated."""
+        rc = _lib().esi_push_events(self.h, int(ptr) if n else None, int(n))
+        if rc == ESI_OK:
+            self._pushed += int(n)
+            self._borrowed.append((keep, self._pushed))
+        return rc
+
+    def pending(self) -> int:
+        """Events pushed but not yet integrated by a render."""
+        return self._pushed - self._consumed
+
+    def _release_consumed(self):
+        self._consumed += self.last_render_stats()["events"]
+        self._borrowed = [(b, end) for (b, end) in self._borrowed if end > self._consumed]
 
     def render(self, t_frame_us: int, out=None):
         if out is None:
             out = np.empty((self.H, self.W), np.uint8)
         _check(render(self.h, t_frame_us, out), "esi_render")
+        self._release_consumed()
         return out
 
     def render_many(self, t_frames_us, out=None):
@@ -209,11 +246,14 @@ class Esi:
         if out is None:
             out = np.empty((len(tf), self.H, self.W), np.uint8)
         _check(render_many(self.h, tf, out), "esi_render_many")
-        self._borrowed = []          # every borrowed buffer consumed up to the last frame
+        self._release_consumed()     # buffers with events after the last frame stay borrowed
         return out
 
     def render_many_rc(self, t_frames_us, out) -> int:
-        return render_many(self.h, t_frames_us, out)
+        rc = render_many(self.h, t_frames_us, out)
+        if rc == ESI_OK:
+            self._release_consumed()
+        return rc
 
     def get_state(self):
         S = np.empty((self.H, self.W), np.float32)
@@ -229,6 +269,7 @@ class Esi:
     def reset(self):
         _check(reset(self.h), "esi_reset")
         self._borrowed = []
+        self._pushed = self._consumed = 0
 
     def set_stream(self, stream_handle: int):
         _check(set_stream(self.h, stream_handle), "esi_set_stream")

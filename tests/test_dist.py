@@ -42,8 +42,79 @@ class OracleBand:
     def get_state(self):
         return self.o.get_state()
 
+    def pending(self):
+        return self.o.pending()
+
     def close(self):
         self.o.close()
+
+
+class FileTransport:
+    """Stand-in for PeerTransport between CPU processes: receive arenas are
+    files mapped by every rank (np.memmap), "P2P stores" are writes into the
+    destination rank's mapping, and the router is the plain stable partition.
+    It exercises RowBandSharded's P2P host logic -- counts all-gather, receive
+    offsets, arena growth and handle exchange, recycling after a render."""
+
+    def __init__(self, root, rank, starts):
+        self.root, self.rank, self.starts = root, rank, starts
+        self.k = 0
+        self.routed = None
+        self.maps = {}
+        self.log = []
+
+    def _map(self, path):
+        if path not in self.maps:
+            self.maps[path] = np.memmap(path, dtype=np.int64, mode="r+").reshape(-1, 2)
+        return self.maps[path]
+
+    def count(self, shard):
+        routed, counts = np_router(shard, self.starts)
+        self.routed = (routed.numpy(), np.concatenate([[0], np.cumsum(counts)]))
+        return counts
+
+    def scatter(self, dst, off):
+        rec, cs = self.routed
+        for g, path in enumerate(dst):
+            n = cs[g + 1] - cs[g]
+            if n:
+                m = self._map(path)
+                assert off[g] + n <= m.shape[0], "write past the destination arena"
+                m[off[g]:off[g] + n] = rec[cs[g]:cs[g + 1]]
+        self.log.append(("scatter", list(off)))
+
+    def sync(self):
+        for m in self.maps.values():
+            m.flush()
+
+    def alloc(self, nrec):
+        path = os.path.join(self.root, f"arena_{self.rank}_{self.k}.bin")
+        self.k += 1
+        np.memmap(path, dtype=np.int64, mode="w+", shape=(nrec, 2)).flush()
+        self.log.append(("alloc", nrec))
+        return path
+
+    def free(self, path):
+        self.maps.pop(path, None)
+        os.remove(path)
+
+    def export(self, path):
+        return path
+
+    def open(self, handle):
+        return handle
+
+    def unmap(self, path):
+        self.maps.pop(path, None)
+
+    def push(self, band, path, off, n):
+        if not n:
+            return 0
+        m = np.memmap(path, dtype=np.int64, mode="r").reshape(-1, 2)
+        return band.push(torch.from_numpy(np.array(m[off:off + n])))
+
+    def close(self):
+        self.maps = {}
 
 
 def np_router(events, starts):
@@ -131,6 +202,54 @@ def test_row_band_sharding_gloo_world2_equals_full_sensor(W, H):
     for rank, frames, stats in res:
         assert np.array_equal(frames, f_ref), f"rank {rank}: assembled frames differ from the full sensor"
         assert stats["received"] > 0 and stats["sent"] > 0
+
+
+def _worker_p2p(rank, world, path, root, W, H, a, tf_list, q):
+    dist.init_process_group("gloo", init_method=f"file://{path}", rank=rank, world_size=world)
+    try:
+        T = FileTransport(root, rank, row_bands(H, world))
+        rb = RowBandSharded(W, H, band_factory=OracleBand, transport=T, device=torch.device("cpu"), **PRM)
+        rb.MIN_ARENA = 64                                  # force arena growth and re-exchange of handles
+        frames = []
+        # rounds of different sizes, two renders (the second reuses the recycled arenas)
+        bounds = [0, 300, 350, 1800, 3000, 3100, 6000]
+        for k in range(len(bounds) - 1):
+            part = a[bounds[k]:bounds[k + 1]]
+            lo, hi = time_shard_bounds(len(part), world)[rank:rank + 2]
+            assert rb.push_shard(from_numpy_struct(part[lo:hi])) == 0
+            if bounds[k + 1] == 3000:
+                frames.append(rb.render_many(tf_list[0]).numpy())
+        frames.append(rb.render_many(tf_list[1]).numpy())
+        q.put((rank, frames, rb.stats, T.log))
+        rb.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_band_p2p_exchange_gloo_world2_equals_full_sensor(tmp_path):
+    W, H = 16, 11
+    a = stream(7, W, H, 6000, 300_000)
+    t_split = int(a["t"][2999])
+    tf_all = np.arange(1, 31, dtype=np.int64) * 10_000
+    tf0 = tf_all[tf_all < t_split]                     # first render: frames before round 4's events
+    tf1 = tf_all[tf_all >= int(a["t"][3099]) + 1]
+    f_ref, _, _ = oracle.run(W, H, a, np.concatenate([tf0, tf1]), **PRM)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    path = tempfile.mktemp()
+    procs = [ctx.Process(target=_worker_p2p, args=(r, 2, path, str(tmp_path), W, H, a, (tf0, tf1), q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, frames, stats, log in res:
+        got = np.concatenate(frames)
+        assert np.array_equal(got, f_ref), f"rank {rank}: P2P-exchanged frames differ from the full sensor"
+        assert stats["received"] > 0 and stats["sent"] > 0
+        assert sum(1 for e in log if e[0] == "alloc") >= 2, "arena growth path not exercised"
 
 
 def _worker_streams(rank, world, path, q):
@@ -244,3 +363,66 @@ def test_band_handles_on_one_gpu_equal_full_sensor(G):
         else:
             assert_frames_close(f_bands, f_full)
             assert_state_close(S_b, T_b, S_full.astype(np.float64), T_full)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,S", [(2, 2), (4, 3), (8, 8)])
+def test_p2p_router_scatter_into_band_arenas(G, S):
+    """The P2P exchange kernel on one GPU: S time shards ("source ranks"), each
+    counted and scattered by esi_router_* straight into G per-band arenas at
+    the offsets RowBandSharded computes (fill + events of earlier sources).
+    Every arena must hold its band's events in arrival order, y rebased: the
+    stable partition of the whole stream (bit-exact).  On the GPU box the
+    arenas of other ranks are IPC mappings; the kernel is the same."""
+    from paper_2508_02238_b200.dist import PeerTransport
+    W, H = 200, 96
+    a = stream(40 + G, W, H, 150_000, 1_000_000)
+    starts = row_bands(H, G)
+    ev = from_numpy_struct(a).cuda()
+    bounds = time_shard_bounds(len(a), S)
+    T = PeerTransport(0, H, starts)
+    ref, c_ref = np_router(from_numpy_struct(a), starts)
+    pad = 5                                                    # arenas start with some fill
+    bufs = [torch.full((int(c_ref[g]) + pad, 2), -1, dtype=torch.int64, device="cuda") for g in range(G)]
+    arenas = [b.data_ptr() for b in bufs]
+    torch.cuda.synchronize()
+    M = []
+    for s in range(S):
+        M.append(T.count(ev[bounds[s]:bounds[s + 1]]))
+        off = np.array([pad + sum(int(M[q][g]) for q in range(s)) for g in range(G)], np.int64)
+        T.scatter(arenas, off)
+        T.sync()
+    assert np.array_equal(np.sum(M, axis=0), c_ref)
+    cs = np.concatenate([[0], np.cumsum(c_ref)])
+    for g in range(G):
+        got = bufs[g].cpu()
+        assert torch.equal(got[:pad], torch.full((pad, 2), -1, dtype=torch.int64)), f"band {g}: prefix touched"
+        assert torch.equal(got[pad:], ref[cs[g]:cs[g + 1]]), f"band {g}"
+    T.close()
+
+
+@pytest.mark.gpu
+def test_ipc_export_of_arena():
+    from paper_2508_02238_b200.dist import PeerTransport
+    T = PeerTransport(0, 8, row_bands(8, 2))
+    p = T.alloc(1024)
+    h = T.export(p)
+    assert isinstance(h, bytes) and len(h) == 64 and any(h)
+    T.free(p)
+    T.close()
+
+
+@pytest.mark.gpu
+def test_borrowed_buffers_kept_while_pending():
+    """Device pushes are borrowed (esi.h): the wrapper keeps the tensor alive
+    while any of its events is still pending after a render."""
+    from paper_2508_02238_b200 import Esi
+    e = Esi(16, 8, **PRM)
+    a = stream(3, 16, 8, 1000, 100_000)
+    ev = from_numpy_struct(a).cuda()
+    assert e.push(ev) == 0
+    e.render_many(np.array([50_000], np.int64))
+    assert e.pending() > 0 and len(e._borrowed) == 1
+    e.render_many(np.array([100_000], np.int64))
+    assert e.pending() == 0 and len(e._borrowed) == 0
+    e.close()
