@@ -34,14 +34,15 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // 16-byte streaming load (read once: evict-first in L1/L2).
 __device__ __forceinline__ int4 ld_stream16(const int4* p) { return __ldcs(p); }
 
-// 8-byte streaming store of frame bytes.
+// 8-byte streaming store of frame bytes (st.global.cs; an intrinsic, not asm
+// volatile with a memory clobber, so independent shared loads may move ahead).
 __device__ __forceinline__ void st_stream8(void* p, uint32_t lo, uint32_t hi) {
-  asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(lo), "r"(hi) : "memory");
+  __stcs(reinterpret_cast<uint2*>(p), make_uint2(lo, hi));
 }
 
 // 4-byte streaming store of frame bytes.
 __device__ __forceinline__ void st_stream4(void* p, uint32_t v) {
-  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  __stcs(reinterpret_cast<unsigned int*>(p), v);
 }
 
 // Eq. 4: d(dt) = max{(1 - k dt)^b, 0}, dt in integer microseconds (>= 0).

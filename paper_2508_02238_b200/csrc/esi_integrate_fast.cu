@@ -47,13 +47,14 @@ struct FastSmem {
   uint16_t* dq;                               // [kSB / 4] dense pixels of the segment
   uint32_t* nd;
   int32_t* wend;                              // [kWinCap] window ends inside the current sub-batch
+  int32_t* wtj;                               // [kWinCap] frame time of each listed window (rel. to trel)
   uint32_t* pre;                              // [n_tiles + 1] band events before tile t
   uint16_t* mo;                               // [n_tiles] offset of the band's run inside tile t
 };
 
 __host__ __device__ inline size_t fast_smem_bytes(int bp, int n_tiles) {
   const size_t b = (size_t)bp;
-  return b * 12 + kSB * 2 + 2 * kSB * 8 + kNW * kStage * 8 + (kSB / 4) * 2 + 16 + kWinCap * 4 +
+  return b * 12 + kSB * 2 + 2 * kSB * 8 + kNW * kStage * 8 + (kSB / 4) * 2 + 16 + 2 * kWinCap * 4 +
          (size_t)(n_tiles + 1) * 4 + (((size_t)n_tiles * 2 + 15) & ~(size_t)15) + 64;
 }
 
@@ -70,6 +71,7 @@ __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_til
   m.mo = reinterpret_cast<uint16_t*>(q); q += ((size_t)n_tiles * 2 + 15) & ~(size_t)15;
   m.nd = reinterpret_cast<uint32_t*>(q); q += 16;
   m.wend = reinterpret_cast<int32_t*>(q); q += kWinCap * 4;
+  m.wtj = reinterpret_cast<int32_t*>(q); q += kWinCap * 4;
   m.next = reinterpret_cast<uint16_t*>(q); q += kSB * 2;
   m.dq = reinterpret_cast<uint16_t*>(q);
   return m;
@@ -93,22 +95,27 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
     const float2 mo = make_float2(c.magic_off, c.magic_off);
     const float4* S4 = reinterpret_cast<const float4*>(sm.S);
     const float4* T4 = reinterpret_cast<const float4*>(sm.T);
-    for (int q = threadIdx.x; q < nq; q += kNT) {
+    auto quad = [&](int q) -> uint32_t {
       const float4 s0 = S4[q], t0 = T4[q];
       float2 w0 = __fadd2_rn(make_float2(t0.x, t0.y), naj), w1 = __fadd2_rn(make_float2(t0.z, t0.w), naj);
       w0.x = fmaxf(w0.x, 0.f); w0.y = fmaxf(w0.y, 0.f); w1.x = fmaxf(w1.x, 0.f); w1.y = fmaxf(w1.y, 0.f);
       const float2 v0 = __fmul2_rn(make_float2(s0.x, s0.y), __fmul2_rn(w0, w0));
       const float2 v1 = __fmul2_rn(make_float2(s0.z, s0.w), __fmul2_rn(w1, w1));
       const float2 r0 = __fadd2_rd(__ffma2_rn(v0, sw2, off), mo), r1 = __fadd2_rd(__ffma2_rn(v1, sw2, off), mo);
-      const uint32_t v = __byte_perm(__byte_perm(__float_as_uint(r0.x), __float_as_uint(r0.y), 0x0040),
-                                     __byte_perm(__float_as_uint(r1.x), __float_as_uint(r1.y), 0x0040), 0x5410);
-      const int base = q * 4;
-      if (vec && base + 4 <= npx) {
-        st_stream4(frame + base, v);
-      } else {
-        const int n = min(4, npx - base);
-        for (int u = 0; u < n; ++u) frame[base + u] = (uint8_t)((v >> (8 * u)) & 0xffu);
-      }
+      return __byte_perm(__byte_perm(__float_as_uint(r0.x), __float_as_uint(r0.y), 0x0040),
+                         __byte_perm(__float_as_uint(r1.x), __float_as_uint(r1.y), 0x0040), 0x5410);
+    };
+    // full quads: one 4-byte streaming store each (__stcs: no memory clobber, so the
+    // next quad's shared loads can be issued ahead); the remainder quads fall on the
+    // last warp (warp 0 also lists the windows)
+    unsigned int* f4 = reinterpret_cast<unsigned int*>(frame);
+    const int nfull = vec ? (npx >> 2) : 0;
+#pragma unroll 2
+    for (int q = kNT - 1 - (int)threadIdx.x; q < nfull; q += kNT) __stcs(f4 + q, quad(q));
+    for (int q = nfull + (int)threadIdx.x; q < nq; q += kNT) {     // ragged tail / unaligned output
+      const uint32_t v = quad(q);
+      const int base = q * 4, n = min(4, npx - base);
+      for (int u = 0; u < n; ++u) frame[base + u] = (uint8_t)((v >> (8 * u)) & 0xffu);
     }
     return;
   }
@@ -148,6 +155,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
   uint2 evr[kEPT];                                        // this thread's events, kept from claim to apply
 #pragma unroll
   for (int r = 0; r < kEPT; ++r) {                        // claim
+    if (e0 + r * kNT >= e1) break;                        // uniform: no thread has an event in this round
     const int i = e0 + tid + r * kNT;
     if (i < e1) {
       evr[r] = sub[i];
@@ -329,7 +337,6 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
   __syncthreads();
 
   int j = f_lo;
-  int32_t tj = (j < f_hi) ? (int32_t)(a.tf[j] - trel) : tcap;
   bool done = false;
   uint32_t gen = 0;
   // ---- 1. gather sub-batch k into sub[k & 1]; sub-batch k+1 is in flight while k is integrated
@@ -347,16 +354,18 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
     bool more = true;
     while (more) {
       more = false;
-      if (warp == 0) {
+      if (warp == 0) {                          // window w ends frame j + w at time wtj[w]
         int e = e0, w = 0, jj = j;
-        int32_t tw = tj;
         while (true) {
+          const int32_t tw = (jj < f_hi) ? (int32_t)(a.tf[jj] - trel) : tcap;
           e += upper_bound_rel<kSB>(sub + e, n_sb - e, trel32, tw, lane);
-          if (lane == 0) sm.wend[w] = e;
+          if (lane == 0) {
+            sm.wend[w] = e;
+            sm.wtj[w] = tw;
+          }
           ++w;
           if (e == n_sb || jj >= f_hi || w == kWinCap - 1) break;
           ++jj;
-          tw = (jj < f_hi) ? (int32_t)(a.tf[jj] - trel) : tcap;
         }
         if (lane == 0) sm.wend[kWinCap - 1] = w;   // count in the last slot (at most kWinCap - 1 windows)
       }
@@ -375,9 +384,8 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
         }
         if (e1 == n_sb) break;                  // the window may continue in the next sub-batch
         if (j >= f_hi) { done = true; break; }  // later events stay pending
-        fast_readout<BM>(a, sm, j, tj, px0, npx, kc);
+        fast_readout<BM>(a, sm, j, sm.wtj[w], px0, npx, kc);
         ++j;
-        tj = (j < f_hi) ? (int32_t)(a.tf[j] - trel) : tcap;
         e0 = e1;
         more = (w == nwin - 1);                 // every listed window closed: list the next ones
       }
