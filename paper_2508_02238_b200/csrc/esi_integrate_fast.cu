@@ -28,9 +28,12 @@ namespace {
 
 #include "esi_fast_common.cuh"
 
-constexpr int kNW = 8;                        // warps per CTA
+#ifndef ESI_K2_WARPS
+#define ESI_K2_WARPS 8
+#endif
+constexpr int kNW = ESI_K2_WARPS;             // warps per CTA
 constexpr int kNT = kNW * 32;                 // threads per CTA
-constexpr int kEPT = kK2Ctas >= 4 ? 4 : 6;    // events per thread per segment (smem budget)
+constexpr int kEPT = (kK2Ctas >= 4 ? 1024 : 1536) / kNT;   // events per thread per segment (smem budget)
 constexpr int kSB = kNT * kEPT;               // events per sub-batch
 constexpr int kStage = (kEPT * 32 + 1) / 2;   // uint2 per warp: kEPT * 32 chain heads (u32)
 constexpr int kWinCap = 32;                   // window ends listed per pass (warp 0, per sub-batch)
@@ -355,19 +358,28 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
     while (more) {
       more = false;
       if (warp == 0) {                          // window w ends frame j + w at time wtj[w]
-        int e = e0, w = 0, jj = j;
-        while (true) {
-          const int32_t tw = (jj < f_hi) ? (int32_t)(a.tf[jj] - trel) : tcap;
-          e += upper_bound_rel<kSB>(sub + e, n_sb - e, trel32, tw, lane);
-          if (lane == 0) {
-            sm.wend[w] = e;
-            sm.wtj[w] = tw;
+        // lane l lists window l: frame j + l, its end = upper bound of t_{j+l} in
+        // [e0, n_sb) (the sub-batch is time-sorted); the list stops at the first
+        // window that reaches the sub-batch end or the last frame
+        const int jj = j + lane;
+        const int32_t tw = (jj < f_hi) ? (int32_t)(a.tf[jj] - trel) : tcap;
+        int base = e0, len = n_sb - e0;
+        while (len > 0) {
+          const int half = len >> 1;
+          if ((int32_t)(sub[base + half].x - trel32) <= tw) {
+            base += half + 1;
+            len -= half + 1;
+          } else {
+            len = half;
           }
-          ++w;
-          if (e == n_sb || jj >= f_hi || w == kWinCap - 1) break;
-          ++jj;
         }
-        if (lane == 0) sm.wend[kWinCap - 1] = w;   // count in the last slot (at most kWinCap - 1 windows)
+        const bool stop = base == n_sb || jj >= f_hi || lane == kWinCap - 2;
+        const int last = __ffs(__ballot_sync(kFull, stop)) - 1;   // lane kWinCap - 2 always stops
+        if (lane <= last) {
+          sm.wend[lane] = base;
+          sm.wtj[lane] = tw;
+        }
+        if (lane == 0) sm.wend[kWinCap - 1] = last + 1;   // count in the last slot
       }
       __syncthreads();
       const int nwin = sm.wend[kWinCap - 1];
