@@ -246,8 +246,9 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
 
 // Gather band events [sb0, min(sb0 + kSB, n_b)) into dst with cp.async: 8 (tile,
 // band) segments per warp step, 4 lanes per segment, tiles in order = arrival order.
+// Warps gw = 0 .. ngw-1 share the copies.
 __device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const uint32_t* pre, const uint16_t* mo,
-                                           int n_tiles, int n_b, int sb0, uint2* dst, int warp, int lane) {
+                                           int n_tiles, int n_b, int sb0, uint2* dst, int gw, int ngw, int lane) {
   const uint32_t q_end = (uint32_t)min(sb0 + kSB, n_b);
   int t_lo = 0;                                 // last tile with pre[t] <= sb0 (32-ary search)
 #pragma unroll
@@ -256,7 +257,7 @@ __device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const 
     const unsigned b = __ballot_sync(kFull, t < n_tiles && pre[t] <= (uint32_t)sb0);
     t_lo += (31 - __clz(b | 1u)) * stride;
   }
-  for (int tb = t_lo + warp * 8; tb < n_tiles; tb += kNW * 8) {
+  for (int tb = t_lo + gw * 8; tb < n_tiles; tb += ngw * 8) {
     if (pre[tb] >= q_end) break;                // segments are in order: the rest is later
     const int t = tb + (lane >> 2);
     uint32_t i0 = 0, i1 = 0, p0 = 0;
@@ -343,13 +344,16 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
   bool done = false;
   uint32_t gen = 0;
   // ---- 1. gather sub-batch k into sub[k & 1]; sub-batch k+1 is in flight while k is integrated
-  if (n_b > 0) gather_sub(a.rec, sm.pre, sm.mo, n_tiles, n_b, 0, sm.sub[0], warp, lane);
+  if (n_b > 0) gather_sub(a.rec, sm.pre, sm.mo, n_tiles, n_b, 0, sm.sub[0], warp, kNW, lane);
   for (int sb0 = 0, kb = 0; sb0 < n_b && !done; sb0 += kSB, ++kb) {
     const int n_sb = min(kSB, n_b - sb0);
     const uint2* sub = (kb & 1) ? sm.sub[1] : sm.sub[0];   // no dynamic index into sm (keeps it in registers)
     cp_async_wait_all();
     __syncthreads();
-    if (sb0 + kSB < n_b) gather_sub(a.rec, sm.pre, sm.mo, n_tiles, n_b, sb0 + kSB, (kb & 1) ? sm.sub[0] : sm.sub[1], warp, lane);
+    // warp 0 lists the first windows meanwhile (the other warps wait for that list)
+    if (sb0 + kSB < n_b && warp > 0)
+      gather_sub(a.rec, sm.pre, sm.mo, n_tiles, n_b, sb0 + kSB, (kb & 1) ? sm.sub[0] : sm.sub[1], warp - 1, kNW - 1,
+                 lane);
     // ---- 2. segments = frame windows inside the sub-batch; readout at each window end.
     // Window ends (events of the sub-batch with t <= t_j) are listed by warp 0,
     // kWinCap at a time, behind one barrier, instead of being searched by every warp.
