@@ -16,6 +16,8 @@ struct esio {
   double C, k, b, s_min, s_max;    /* Alg. 2 inputs k, b, C; Eq. 13 bounds */
   int64_t t_origin;
   int32_t readout_decay;
+  int32_t decay_kind;              /* 0: Eq. 4 (ESI); 1: exponential (camera plugin) */
+  int32_t decay_first;             /* 0: Alg. 2 order (add, then decay); 1: decay, then add (A1 variant) */
   double* S;                       /* accumulation matrix */
   int64_t* T;                      /* last decay time matrix */
   int64_t* pt; uint16_t* px; uint16_t* py; int8_t* pp;   /* pending events */
@@ -31,6 +33,20 @@ double esio_decay(int64_t dt_us, double k, double b) {
   double u = 1.0 - k * dt_s;
   if (u > 0.0) return pow(u, b);
   return 0.0;
+}
+
+/* Exponential decay of the DV "Accumulator" camera plugin that the paper
+ * compares against ("the exponential function used in the
+ * camera plugin"); Algorithm 1 with d(t) replaced by
+ * exp(-lambda t), lambda = k here.  t = dt_us * 1e-6 s (A11). */
+double esio_decay_exp(int64_t dt_us, double k) {
+  double dt_s = (double)dt_us / 1e6;
+  return exp(-k * dt_s);
+}
+
+/* The handle's decay function (Eq. 4, or the exponential variant). */
+static double esio_decay_h(const esio_t* h, int64_t dt_us) {
+  return h->decay_kind ? esio_decay_exp(dt_us, h->k) : esio_decay(dt_us, h->k, h->b);
 }
 
 /* Eq. 13: S = min(max(S, S_min), S_max). */
@@ -135,14 +151,29 @@ int esio_push(esio_t* h, const int64_t* t, const uint16_t* x, const uint16_t* y,
   return ESIO_OK;
 }
 
-/* One pass of the Alg. 2 loop body for event e_i at pixel (x, y). */
+/* One pass of the Alg. 2 loop body for event e_i at pixel (x, y).
+ * decay_first (reading A1 variant; the order of Eq. 3/5 and of the
+ * complementary filter): the decay line runs before
+ * the contrast step; everything else is unchanged. */
 static void esio_apply_event(esio_t* h, int64_t t, uint16_t x, uint16_t y, int8_t p) {
   size_t i = (size_t)y * (size_t)h->W + (size_t)x;
-  h->S[i] = h->S[i] + (double)p * h->C;                 /* P:243  S <- S + p_i x C        */
   int64_t dt = t - h->T[i];                             /* P:245  dt <- t_i - T(x, y)     */
-  h->S[i] = h->S[i] * esio_decay(dt, h->k, h->b);       /* P:247  S <- S x max{(1-k dt)^b, 0} */
+  if (!h->decay_first) {
+    h->S[i] = h->S[i] + (double)p * h->C;               /* P:243  S <- S + p_i x C        */
+    h->S[i] = h->S[i] * esio_decay_h(h, dt);            /* P:247  S <- S x max{(1-k dt)^b, 0} */
+  } else {
+    h->S[i] = h->S[i] * esio_decay_h(h, dt);            /* P:247 first                    */
+    h->S[i] = h->S[i] + (double)p * h->C;               /* then P:243                     */
+  }
   h->T[i] = t;                                          /* P:249  T <- t_i                */
   h->S[i] = esio_clamp(h->S[i], h->s_min, h->s_max);    /* P:251  clamp (Eq. 13)          */
+}
+
+int esio_set_variant(esio_t* h, int32_t decay_kind, int32_t decay_first) {
+  if (!h || decay_kind < 0 || decay_kind > 1 || decay_first < 0 || decay_first > 1) return ESIO_ERR_INVALID_ARG;
+  h->decay_kind = decay_kind;
+  h->decay_first = decay_first;
+  return ESIO_OK;
 }
 
 /* Integrate pending events with t <= t_limit (A6: ties belong to the frame). */
@@ -172,7 +203,7 @@ int esio_render(esio_t* h, int64_t t_frame, uint8_t* out) {
   size_t P = (size_t)h->W * (size_t)h->H;
   for (size_t i = 0; i < P; i++) {
     double v = h->S[i];
-    if (h->readout_decay) v = v * esio_decay(t_frame - h->T[i], h->k, h->b);
+    if (h->readout_decay) v = v * esio_decay_h(h, t_frame - h->T[i]);
     v = esio_clamp(v, h->s_min, h->s_max);
     out[i] = esio_map(v, h->s_min, h->s_max);
   }

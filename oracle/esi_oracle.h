@@ -42,11 +42,16 @@ typedef struct esio esio_t;
 
 /* Eq. 4: d(dt) = max{(1 - k*dt)^b, 0}, dt in integer microseconds. */
 double esio_decay(int64_t dt_us, double k, double b);
+/* exp(-k dt): the exponential decay variant. */
+double esio_decay_exp(int64_t dt_us, double k);
 /* Eq. 13 */
 double esio_clamp(double v, double s_min, double s_max);
 /* Eq. 14, rounded half away from zero, saturated to [0,255]. */
 uint8_t esio_map(double v, double s_min, double s_max);
 
+/* Decay variants: decay_kind 0 = Eq. 4, 1 = exp(-k dt);
+ * decay_first 0 = Alg. 2 order (add, then decay), 1 = decay, then add. */
+int esio_set_variant(esio_t* h, int32_t decay_kind, int32_t decay_first);
 int esio_create(int32_t width, int32_t height, double C, double k, double b,
                 double s_min, double s_max, int64_t t_origin,
                 int32_t readout_decay, esio_t** out);

@@ -52,6 +52,8 @@ def lib():
         i32, i64, u64, dbl, vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t,
                                   ctypes.c_double, ctypes.c_void_p)
         L.esio_decay.argtypes = [i64, dbl, dbl]; L.esio_decay.restype = dbl
+        L.esio_decay_exp.argtypes = [i64, dbl]; L.esio_decay_exp.restype = dbl
+        L.esio_set_variant.argtypes = [vp, i32, i32]; L.esio_set_variant.restype = ctypes.c_int
         L.esio_clamp.argtypes = [dbl, dbl, dbl]; L.esio_clamp.restype = dbl
         L.esio_map.argtypes = [dbl, dbl, dbl]; L.esio_map.restype = ctypes.c_uint8
         L.esio_create.argtypes = [i32, i32, dbl, dbl, dbl, dbl, dbl, i64, i32, ctypes.POINTER(vp)]
@@ -109,7 +111,7 @@ class Oracle:
     """Stateful oracle handle (same call structure as the C ABI)."""
 
     def __init__(self, width, height, C=0.15, k=10.0, b=2.0, s_min=-1.5, s_max=1.5,
-                 t_origin=0, readout_decay=1):
+                 t_origin=0, readout_decay=1, decay_kind=0, decay_first=0):
         self.W, self.H = int(width), int(height)
         self.P = self.W * self.H
         h = ctypes.c_void_p()
@@ -118,6 +120,9 @@ class Oracle:
         if rc:
             raise OracleError(rc, "esio_create")
         self._h = h
+        rc = lib().esio_set_variant(h, int(decay_kind), int(decay_first))
+        if rc:
+            raise OracleError(rc, "esio_set_variant")
 
     def close(self):
         if getattr(self, "_h", None):
@@ -167,8 +172,18 @@ class Oracle:
 
 
 def run(width, height, events, t_frames, C=0.15, k=10.0, b=2.0, s_min=-1.5, s_max=1.5,
-        t_origin=0, readout_decay=1):
+        t_origin=0, readout_decay=1, decay_kind=0, decay_first=0):
     """Whole-stream oracle: returns (frames[F,H,W] u8, S[H,W] f64, T[H,W] i64)."""
+    if decay_kind or decay_first:                 # variants: through the handle
+        o = Oracle(width, height, C=C, k=k, b=b, s_min=s_min, s_max=s_max, t_origin=t_origin,
+                   readout_decay=readout_decay, decay_kind=decay_kind, decay_first=decay_first)
+        rc = o.push(events)
+        if rc:
+            raise OracleError(rc, "esio_push")
+        frames = o.render_many(t_frames)
+        S, T = o.get_state()                      # as esio_run: events after the last frame stay pending
+        o.close()
+        return frames, S, T
     t, x, y, p = _soa(events)
     tf = np.ascontiguousarray(t_frames, dtype=np.int64)
     P = int(width) * int(height)
@@ -192,13 +207,15 @@ def stable_group_by(keys) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # Pure-Python restatement of Algorithm 2 for small inputs.
 # ---------------------------------------------------------------------------
-def _py_decay(dt_us, k, b):
+def _py_decay(dt_us, k, b, kind=0):
+    if kind:
+        return math.exp(-k * (dt_us / 1e6))   # exponential variant
     u = 1.0 - k * (dt_us / 1e6)           # Eq. 4
     return u ** b if u > 0.0 else 0.0
 
 
 def py_run(width, height, events, t_frames, C=0.15, k=10.0, b=2.0, s_min=-1.5, s_max=1.5,
-           t_origin=0, readout_decay=1):
+           t_origin=0, readout_decay=1, decay_kind=0, decay_first=0):
     t, x, y, p = _soa(events)
     S = [0.0] * (width * height)
     T = [int(t_origin)] * (width * height)       # P:239 (A3)
@@ -208,15 +225,19 @@ def py_run(width, height, events, t_frames, C=0.15, k=10.0, b=2.0, s_min=-1.5, s
     for tf in t_frames:
         while i < n and int(t[i]) <= int(tf):     # A6: t == t_frame belongs to the frame
             q = int(y[i]) * width + int(x[i])
-            S[q] = S[q] + int(p[i]) * C
             dt = int(t[i]) - T[q]
-            S[q] = S[q] * _py_decay(dt, k, b)
+            if decay_first:                                           # variant: P:247 then P:243
+                S[q] = S[q] * _py_decay(dt, k, b, decay_kind)
+                S[q] = S[q] + int(p[i]) * C
+            else:
+                S[q] = S[q] + int(p[i]) * C
+                S[q] = S[q] * _py_decay(dt, k, b, decay_kind)
             T[q] = int(t[i])
             S[q] = min(max(S[q], s_min), s_max)
             i += 1
         fr = np.empty(width * height, np.uint8)
         for q in range(width * height):
-            v = S[q] * _py_decay(int(tf) - T[q], k, b) if readout_decay else S[q]
+            v = S[q] * _py_decay(int(tf) - T[q], k, b, decay_kind) if readout_decay else S[q]
             v = min(max(v, s_min), s_max)
             qv = 255.0 * (v - s_min) / (s_max - s_min)                # Eq. 14
             r = math.floor(qv + 0.5) if qv >= 0 else math.ceil(qv - 0.5)

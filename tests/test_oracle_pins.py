@@ -433,3 +433,75 @@ def test_pure_python_copy_agrees_on_small_inputs():
         f1, S1, T1 = oracle.py_run(6, 4, (t, x, y, p), tf, b=b, s_min=-0.4, s_max=0.5)
         assert np.array_equal(f0, f1) and np.array_equal(T0, T1)
         assert np.max(np.abs(S0 - S1)) < 1e-12
+
+
+# ---------------------------------------------------------------- P14: decay variants
+def test_exp_decay_spec_examples_and_exponent_law():
+    """SPEC S:261-263 (expdecay_process examples): dt = 0 -> 1; lambda = 10,
+    dt = 0.1 s -> e^-1; n-step compounding equals one long decay (the
+    structural contrast to ESI's Eq. 6)."""
+    L = oracle.lib()
+    assert L.esio_decay_exp(0, 10.0) == 1.0
+    assert L.esio_decay_exp(100_000, 10.0) == pytest.approx(math.exp(-1.0), rel=1e-15)
+    rng = np.random.default_rng(21)
+    for _ in range(2000):
+        lam = float(rng.uniform(0.1, 50))
+        a, c = int(rng.integers(0, 200_000)), int(rng.integers(0, 200_000))
+        assert abs(L.esio_decay_exp(a, lam) * L.esio_decay_exp(c, lam) - L.esio_decay_exp(a + c, lam)) < 1e-12
+        n = int(rng.integers(2, 9))
+        assert L.esio_decay_exp(a, lam) ** n == pytest.approx(L.esio_decay_exp(n * a, lam), rel=1e-12)
+
+
+def test_complementary_filter_spec_example():
+    """alpha = 5, two +1 events 0.2 s apart, C = 0.15, decay then add
+    -> 0.15 e^-1 + 0.15 = 0.2052 (exp decay, decay_first)."""
+    o = Oracle(1, 1, C=0.15, k=5.0, b=2.0, s_min=-1.5, s_max=1.5, decay_kind=1, decay_first=1)
+    o.push(ev([(1_000_000, 0, 0, 1), (1_200_000, 0, 0, 1)]))
+    o.flush()
+    S = o.get_state()[0][0, 0]
+    assert S == pytest.approx(0.15 * math.exp(-1.0) + 0.15, rel=1e-14)
+    assert round(S, 4) == 0.2052
+    # SPEC S:270: a single +1 event -> value C at the event time
+    o2 = Oracle(1, 1, C=0.15, k=5.0, decay_kind=1, decay_first=1)
+    o2.push(ev([(300_000, 0, 0, 1)]))
+    assert o2.render(300_000)[0] == math.floor(255 * (0.15 + 1.5) / 3.0 + 0.5)
+    o2.flush()
+    assert o2.get_state()[0][0, 0] == 0.15
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("first", [0, 1])
+def test_variant_geometric_closed_forms(kind, first):
+    """Evenly spaced (D) same-polarity events from the origin, q = d(D):
+    add-then-decay (Alg. 2): S_n = C q (1 - q^n) / (1 - q);
+    decay-then-add:          S_n = C (1 - q^n) / (1 - q)
+    (sums of a geometric series; q = (1 - kD)^b or e^{-kD})."""
+    C, k, b, D = 0.15, 10.0, 2.0, 10_000
+    q = math.exp(-k * D / 1e6) if kind else (1 - k * D / 1e6) ** b
+    o = Oracle(1, 1, C=C, k=k, b=b, s_min=-5.0, s_max=5.0, decay_kind=kind, decay_first=first)
+    for n in range(1, 120):
+        o.push(ev([(D * n, 0, 0, 1)]))
+        o.flush()
+        S = o.get_state()[0][0, 0]
+        want = C * (1 - q ** n) / (1 - q) * (1.0 if first else q)
+        assert S == pytest.approx(want, rel=1e-12, abs=1e-14), (n, S, want)
+
+
+def test_esi_decay_first_two_events():
+    """Eq. 4 decay then add, two +1 events 0.05 s apart at k = 10, b = 2:
+    S = C (1 - 0.5)^2 + C = 1.25 C (first event: 0 * d + C)."""
+    o = Oracle(1, 1, C=0.15, k=10.0, b=2.0, decay_first=1)
+    o.push(ev([(20_000, 0, 0, 1), (70_000, 0, 0, 1)]))
+    o.flush()
+    assert o.get_state()[0][0, 0] == pytest.approx(0.15 * 1.25, rel=1e-15)
+
+
+@pytest.mark.parametrize("kind,first", [(1, 0), (0, 1), (1, 1)])
+def test_variant_pure_python_copy_agrees(kind, first):
+    rng = np.random.default_rng(30 + 2 * kind + first)
+    t, x, y, p = _random_stream(rng, 6, 4, 3000, 300_000)
+    tf = np.arange(1, 31) * 10_000
+    f0, S0, T0 = oracle.run(6, 4, (t, x, y, p), tf, s_min=-0.4, s_max=0.5, decay_kind=kind, decay_first=first)
+    f1, S1, T1 = oracle.py_run(6, 4, (t, x, y, p), tf, s_min=-0.4, s_max=0.5, decay_kind=kind, decay_first=first)
+    assert np.array_equal(f0, f1) and np.array_equal(T0, T1)
+    assert np.max(np.abs(S0 - S1)) < 1e-12
