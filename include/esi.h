@@ -71,6 +71,16 @@ typedef struct {
   int32_t device;        /* CUDA device ordinal                                            */
   int32_t validate_on_push; /* 1: eager, atomic validation in esi_push_events (see above) */
   int32_t chunk_events;  /* events per pipeline chunk; 0 = default (8 Mi)                  */
+  /* Decay variants (reading A20), default 0 = ESI:
+   * decay_kind  0: Eq. 4 d = max{(1 - k dt)^b, 0};  1: d = exp(-k dt), the
+   *             exponential decay of the camera plugin the paper compares
+   *             against (b is ignored).  The device paths
+   *             take d = 0 for k dt >= 24 (e^-24 = 3.8e-11).
+   * decay_first 0: Alg. 2 order, S <- clamp((S + pC) d);
+   *             1: decay, then add, S <- clamp(S d + pC)  (the Eq. 3/5 and
+   *             complementary-filter order, reading A1). */
+  int32_t decay_kind;
+  int32_t decay_first;
 } esi_params_t;
 
 typedef struct esi_handle esi_handle_t;

@@ -51,6 +51,11 @@ __device__ __forceinline__ void st_stream4(void* p, uint32_t v) {
 // (= ceil(1e6/k)) gives d = 0 exactly (reading A14).
 __device__ __forceinline__ float esi_decay(int64_t dt, const DecayParams& dp) {
   if (dt >= dp.dt_cut) return 0.f;
+  if (dp.bmode == kDecayExp) {       // exponential variant (A20): exp(-k dt)
+    if (dp.use_f64) return (float)exp(-dp.k_us * (double)dt);
+    const float f = (float)(int32_t)dt;
+    return expf(-fmaf(f, dp.kh, f * dp.kl));
+  }
   float u;
   if (dp.use_f64) {
     u = (float)(1.0 - dp.k_us * (double)dt);
@@ -65,6 +70,7 @@ __device__ __forceinline__ float esi_decay(int64_t dt, const DecayParams& dp) {
     case 2: return u * u;
     case 3: return u * u * u;
     case 4: { const float u2 = u * u; return u2 * u2; }
+    case kDecayExp: return 0.f;   // not reached: handled above
     default: return u > 0.f ? exp2f(dp.b * log2f(u)) : 0.f;
   }
 }

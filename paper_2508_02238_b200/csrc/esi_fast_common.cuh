@@ -18,6 +18,7 @@ struct FastConst {
   int32_t tau_int;                     // tau is an integer (tau_l == 0)
   int32_t fold;                        // readout mode: 1 = folded (b = 2, readout decay, no clamp, integer tau)
   int32_t rd, cl;                      // readout decay; readout clamp needed (bounds exclude 0)
+  float dtc;                           // exponential variant: d = 0 for dt >= dtc (k dt >= 24)
 };
 
 __device__ __forceinline__ FastConst make_const(const IntArgs& a) {
@@ -38,7 +39,8 @@ __device__ __forceinline__ FastConst make_const(const IntArgs& a) {
   c.tau_int = a.dp.tau_l == 0.f;
   c.rd = a.mp.readout_decay != 0;
   c.cl = !(a.mp.smin <= 0.f && a.mp.smax >= 0.f);
-  c.fold = a.dp.bmode == 2 && c.rd && !c.cl && c.tau_int;
+  c.fold = a.dp.bmode == 2 && c.rd && !c.cl && c.tau_int;   // readout only: independent of the order
+  c.dtc = (float)a.dp.dt_cut;          // < 2^23 on the fast path: exact
   return c;
 }
 
@@ -52,11 +54,25 @@ __device__ __forceinline__ float decay_u(float dt, const FastConst& c) {
   return fmaxf(fmaf(c.kh, w, c.kl * w), 0.f);
 }
 
+// Kernel variant BM = decay kind (0: exp2(b log2 u), 2: b = 2, kDecayExp) + kFirst
+// for the decay-then-add order; both compile-time, so the default path is unchanged.
+constexpr int kFirst = 16;
+
 template <int BM>
 __device__ __forceinline__ float ev_decay(float dt, const FastConst& c) {
+  constexpr int K = BM & (kFirst - 1);
+  if (K == kDecayExp)                  // exponential variant (A20): exp(-k dt), 0 from k dt >= 24 on
+    return dt >= c.dtc ? 0.f : expf(-fmaf(c.kh, dt, c.kl * dt));
   const float u = decay_u(dt, c);
-  if (BM == 2) return u * u;
+  if (K == 2) return u * u;
   return exp2f(c.b * __log2f(u));      // log2(0) = -inf -> d = 0
+}
+
+// One event's update of the state s before the clamp: Alg. 2
+// S <- (S + p C) d, or the decay-then-add variant S <- S d + p C.
+template <int BM>
+__device__ __forceinline__ float ev_update(float s, float pc, float d) {
+  return (BM & kFirst) ? fmaf(s, d, pc) : (s + pc) * d;
 }
 
 // Eq. 13 clamp of one event's result.
@@ -78,13 +94,7 @@ __device__ __forceinline__ uint32_t readout2(float2 s, float2 T, float tj, float
     x = __ffma2_rn(v, make_float2(c.scale_w2, c.scale_w2), make_float2(c.off_frac, c.off_frac));
   } else {
     float2 v = s;
-    if (c.rd) {
-      const float dx = decay_u(tj - T.x, c), dy = decay_u(tj - T.y, c);
-      float2 d;
-      if (BM == 2) d = make_float2(dx * dx, dy * dy);
-      else d = make_float2(exp2f(c.b * __log2f(dx)), exp2f(c.b * __log2f(dy)));
-      v = __fmul2_rn(s, d);
-    }
+    if (c.rd) v = __fmul2_rn(s, make_float2(ev_decay<BM>(tj - T.x, c), ev_decay<BM>(tj - T.y, c)));
     if (c.cl) {
       v.x = fminf(fmaxf(v.x, c.smin), c.smax);
       v.y = fminf(fmaxf(v.y, c.smin), c.smax);
@@ -107,8 +117,8 @@ __device__ __forceinline__ void apply_event(float* S, float* T, int px, uint2 ev
                                             const FastConst& k) {
   const float te = (float)(int32_t)(ev.x - trel);
   const float pc = ((int32_t)ev.y < 0) ? -k.C : k.C;
-  float s = S[px] + pc;                                   // S <- S + p C
-  s *= ev_decay<BM>(te - T[px], k);                       // S <- S max{(1 - k dt)^b, 0}
+  // S <- S + p C; S <- S max{(1 - k dt)^b, 0} (or the variant's order / decay)
+  const float s = ev_update<BM>(S[px], pc, ev_decay<BM>(te - T[px], k));
   S[px] = clampS(s, k);                                   // S <- min(max(S, S_min), S_max)
   T[px] = te;                                             // T <- t
 }
@@ -141,7 +151,7 @@ __device__ __forceinline__ void dense_pixel_apply(float* S, float* T, const uint
     const bool act = lane < nk;
     const float d = act ? ev_decay<BM>(te - tp, k) : 1.f;
     const float pc = ((int32_t)cev.y < 0) ? -k.C : k.C;
-    float fa = d, fc = act ? d * pc : 0.f, flo = k.smin, fhi = k.smax;
+    float fa = d, fc = act ? ((BM & kFirst) ? pc : d * pc) : 0.f, flo = k.smin, fhi = k.smax;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const float ga = __shfl_up_sync(kFull, fa, off), gc = __shfl_up_sync(kFull, fc, off);

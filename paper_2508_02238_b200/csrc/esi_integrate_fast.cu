@@ -227,7 +227,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
       const uint2 e = sub[e0 + iq];
       const float te = (float)(int32_t)(e.x - trel);
       const float pc = ((int32_t)e.y < 0) ? -k.C : k.C;
-      s = clampS((s + pc) * ev_decay<BM>(te - t, k), k);     // Alg. 2 body
+      s = clampS(ev_update<BM>(s, pc, ev_decay<BM>(te - t, k)), k);   // Alg. 2 body
       t = te;
     }
     sm.S[px] = s;
@@ -444,7 +444,13 @@ cudaError_t launch_fast_b(const IntArgs& a, cudaStream_t s) {
 size_t integrate_fast_smem_bytes(int band_px, int n_tiles) { return fast_smem_bytes(band_px, n_tiles); }
 
 cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s) {
-  return a.dp.bmode == 2 ? launch_fast_b<2>(a, s) : launch_fast_b<0>(a, s);
+  if (a.dp.first)
+    return a.dp.bmode == 2           ? launch_fast_b<2 + kFirst>(a, s)
+           : a.dp.bmode == kDecayExp ? launch_fast_b<kDecayExp + kFirst>(a, s)
+                                     : launch_fast_b<kFirst>(a, s);
+  return a.dp.bmode == 2           ? launch_fast_b<2>(a, s)
+         : a.dp.bmode == kDecayExp ? launch_fast_b<kDecayExp>(a, s)
+                                   : launch_fast_b<0>(a, s);
 }
 
 }  // namespace esi

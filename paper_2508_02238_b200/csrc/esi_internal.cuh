@@ -39,12 +39,15 @@ constexpr int kK2Ctas = ESI_K2_CTAS;
 // so that the earliest offending event wins (same as the oracle's first error).
 constexpr unsigned long long kNoError = ~0ull;
 
+constexpr int kDecayExp = 5;   // DecayParams::bmode of the exponential variant (decay_kind 1)
+
 struct DecayParams {
   float kh, kl;          // k * 1e-6 split into a float pair (u = 1 - k dt, dt in us)
   double k_us;           // k * 1e-6 in double (fallback when dt_cut > 2^24)
   int64_t dt_cut;        // smallest dt (us) with 1 - k dt <= 0: ceil(1e6 / k)
   int32_t use_f64;
-  int32_t bmode;         // 1,2,3,4: integer b fast path; 0: exp2(b log2 u)
+  int32_t bmode;         // 1,2,3,4: integer b fast path; 0: exp2(b log2 u); kDecayExp: exp(-k dt)
+  int32_t first;         // 1: decay, then add (variant); 0: Alg. 2 order
   float b;
   // fast K2: u = kf * ((tau_h - dt) + tau_l) with tau = 1e6/k us = tau_h + tau_l
   float tau_h, tau_l, kf;
@@ -69,6 +72,7 @@ struct WideParams {
   double C, k_us, b, smin, smax, scale, off5;
   int64_t dt_cut;
   int32_t bmode, readout_decay;
+  int32_t first;
 };
 
 struct PartArgs {

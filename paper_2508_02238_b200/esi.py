@@ -39,7 +39,8 @@ class EsiParams(ctypes.Structure):
                 ("s_min", ctypes.c_double), ("s_max", ctypes.c_double),
                 ("t_origin_us", ctypes.c_int64), ("readout_decay", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("validate_on_push", ctypes.c_int32),
-                ("chunk_events", ctypes.c_int32)]
+                ("chunk_events", ctypes.c_int32), ("decay_kind", ctypes.c_int32),
+                ("decay_first", ctypes.c_int32)]
 
 
 class EsiError(RuntimeError):

@@ -434,3 +434,45 @@ def test_pinned_host_pipeline_equals_device_path():
         assert np.array_equal(S, S0) and np.array_equal(T, T0), mode
     ref, S_ref, T_ref = oracle_run(w.W, w.H, ev_np_of(w)[to_numpy_struct(w.events)["t"] <= tf[-1]], tf, w.params)
     assert_frames_close(f0, ref)
+
+
+# ---------------------------------------------------------------- decay variants
+@pytest.mark.parametrize("kind,first", [(1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("k", [10.0, 40.0, 0.05])
+@pytest.mark.parametrize("rd", [1, 0])
+def test_decay_variants_against_oracle(kind, first, k, rd):
+    """Exponential decay and/or decay-then-add (reading A20) on the fast path
+    (k = 10, 40 /s) and the fp64 wide path (k = 0.05 /s: horizon > 2^23 us),
+    with a hot pixel (dense path) and small chunks (state carried across)."""
+    ev = random_stream(int(100 * kind + 10 * first + k + rd), 40, 30, 60_000, 600_000, hot=0.03)
+    prm = dict(DEF, k=k, decay_kind=kind, decay_first=first)
+    tf = np.arange(1, 61, dtype=np.int64) * 10_000
+    check(40, 30, ev, tf, prm, readout_decay=rd, chunk_events=16384)
+
+
+@pytest.mark.parametrize("kind,first", [(1, 0), (1, 1), (0, 1)])
+def test_decay_variants_readout_only_frames(kind, first):
+    """Frames rendered with nothing pending (readout-only kernel) use the same decay."""
+    from paper_2508_02238_b200 import Esi
+    W, H = 37, 11
+    ev = random_stream(5 + kind + first, W, H, 20_000, 200_000)
+    prm = dict(DEF, decay_kind=kind, decay_first=first)
+    tf1 = np.arange(1, 21, dtype=np.int64) * 10_000
+    tf2 = 200_000 + np.arange(1, 11, dtype=np.int64) * 7_000
+    f_ref, S_ref, T_ref = oracle_run(W, H, ev, np.concatenate([tf1, tf2]), prm)
+    e = Esi(W, H, **prm)
+    assert e.push(from_numpy_struct(ev).cuda()) == 0
+    f1 = e.render_many(tf1)
+    f2 = e.render_many(tf2)
+    S, T = e.get_state()
+    e.close()
+    assert_frames_close(np.concatenate([f1, f2]), f_ref)
+    assert_state_close(S, T, S_ref, T_ref)
+
+
+def test_decay_variant_params_validated():
+    from paper_2508_02238_b200 import Esi, EsiError
+    for bad in (dict(decay_kind=2), dict(decay_first=-1), dict(decay_kind=-1)):
+        with pytest.raises(EsiError) as ei:
+            Esi(8, 8, **bad)
+        assert ei.value.code == 1
