@@ -243,6 +243,8 @@ def main():
         time.sleep(0.5)
         step()
         torch.cuda.synchronize()
+        barrier(world)              # timed region bracketed by barrier + synchronize on both sides
+        torch.cuda.synchronize()
         t_wall0 = time.time()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -250,6 +252,7 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         clk.mark(t_wall0, time.time())
+        barrier(world)
         # Per-kernel launch durations: a second timed pass of the same steps with a
         # CUDA event pair around every launch, each on the stream the kernel is
         # launched on.  Kept out of the main timed region because the per-launch
