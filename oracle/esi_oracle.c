@@ -16,7 +16,8 @@ struct esio {
   double C, k, b, s_min, s_max;    /* Alg. 2 inputs k, b, C; Eq. 13 bounds */
   int64_t t_origin;
   int32_t readout_decay;
-  int32_t decay_kind;              /* 0: Eq. 4 (ESI); 1: exponential (camera plugin) */
+  int32_t decay_kind;              /* 0: Eq. 4 (ESI); 1: exponential (camera plugin);
+                                      2: none -- the naive Eq. 2 integrator, no per-event clamp */
   int32_t decay_first;             /* 0: Alg. 2 order (add, then decay); 1: decay, then add (A1 variant) */
   double* S;                       /* accumulation matrix */
   int64_t* T;                      /* last decay time matrix */
@@ -46,6 +47,7 @@ double esio_decay_exp(int64_t dt_us, double k) {
 
 /* The handle's decay function (Eq. 4, or the exponential variant). */
 static double esio_decay_h(const esio_t* h, int64_t dt_us) {
+  if (h->decay_kind == 2) return 1.0;   /* Eq. 2: L~(t) = c sum e(s), no decay */
   return h->decay_kind ? esio_decay_exp(dt_us, h->k) : esio_decay(dt_us, h->k, h->b);
 }
 
@@ -166,11 +168,12 @@ static void esio_apply_event(esio_t* h, int64_t t, uint16_t x, uint16_t y, int8_
     h->S[i] = h->S[i] + (double)p * h->C;               /* then P:243                     */
   }
   h->T[i] = t;                                          /* P:249  T <- t_i                */
-  h->S[i] = esio_clamp(h->S[i], h->s_min, h->s_max);    /* P:251  clamp (Eq. 13)          */
+  if (h->decay_kind != 2)                               /* Eq. 2 has no clamp */
+    h->S[i] = esio_clamp(h->S[i], h->s_min, h->s_max);  /* P:251  clamp (Eq. 13)          */
 }
 
 int esio_set_variant(esio_t* h, int32_t decay_kind, int32_t decay_first) {
-  if (!h || decay_kind < 0 || decay_kind > 1 || decay_first < 0 || decay_first > 1) return ESIO_ERR_INVALID_ARG;
+  if (!h || decay_kind < 0 || decay_kind > 2 || decay_first < 0 || decay_first > 1) return ESIO_ERR_INVALID_ARG;
   h->decay_kind = decay_kind;
   h->decay_first = decay_first;
   return ESIO_OK;

@@ -49,7 +49,9 @@ double esio_clamp(double v, double s_min, double s_max);
 /* Eq. 14, rounded half away from zero, saturated to [0,255]. */
 uint8_t esio_map(double v, double s_min, double s_max);
 
-/* Decay variants: decay_kind 0 = Eq. 4, 1 = exp(-k dt);
+/* Decay variants: decay_kind 0 = Eq. 4, 1 = exp(-k dt),
+ * 2 = none with no per-event clamp (the naive Eq. 2 integrator; frames
+ * still clamp at render);
  * decay_first 0 = Alg. 2 order (add, then decay), 1 = decay, then add. */
 int esio_set_variant(esio_t* h, int32_t decay_kind, int32_t decay_first);
 int esio_create(int32_t width, int32_t height, double C, double k, double b,

@@ -208,6 +208,8 @@ def stable_group_by(keys) -> np.ndarray:
 # Pure-Python restatement of Algorithm 2 for small inputs.
 # ---------------------------------------------------------------------------
 def _py_decay(dt_us, k, b, kind=0):
+    if kind == 2:
+        return 1.0                            # Eq. 2: no decay
     if kind:
         return math.exp(-k * (dt_us / 1e6))   # exponential variant
     u = 1.0 - k * (dt_us / 1e6)           # Eq. 4
@@ -233,7 +235,8 @@ def py_run(width, height, events, t_frames, C=0.15, k=10.0, b=2.0, s_min=-1.5, s
                 S[q] = S[q] + int(p[i]) * C
                 S[q] = S[q] * _py_decay(dt, k, b, decay_kind)
             T[q] = int(t[i])
-            S[q] = min(max(S[q], s_min), s_max)
+            if decay_kind != 2:                                       # Eq. 2: no clamp
+                S[q] = min(max(S[q], s_min), s_max)
             i += 1
         fr = np.empty(width * height, np.uint8)
         for q in range(width * height):

@@ -505,3 +505,42 @@ def test_variant_pure_python_copy_agrees(kind, first):
     f1, S1, T1 = oracle.py_run(6, 4, (t, x, y, p), tf, s_min=-0.4, s_max=0.5, decay_kind=kind, decay_first=first)
     assert np.array_equal(f0, f1) and np.array_equal(T0, T1)
     assert np.max(np.abs(S0 - S1)) < 1e-12
+
+
+# ---------------------------------------------------------------- P15: Eq. 2 naive integrator
+def test_naive_integrator_spec_examples_and_pathology():
+    """SPEC S:253-255 (naive_process): +1 then -1 cancel exactly; n equal
+    events give n C; on a pure-noise stream |S| at the worst pixel leaves any
+    fixed bound (random walk, the Fig. 4 pathology) while ESI's state
+    stays inside [S_min, S_max]; frames clamp at render time."""
+    o = Oracle(1, 1, C=0.15, decay_kind=2)
+    o.push(ev([(10, 0, 0, 1), (20, 0, 0, -1)]))
+    o.flush()
+    assert o.get_state()[0][0, 0] == 0.0
+    o2 = Oracle(1, 1, C=0.15, decay_kind=2)
+    o2.push(ev([(10 * i, 0, 0, 1) for i in range(1, 41)]))
+    o2.flush()
+    assert o2.get_state()[0][0, 0] == pytest.approx(40 * 0.15, rel=1e-14)    # 6.0 > S_max: no clamp
+    assert o2.render(1_000_000)[0] == 255                                    # clamped at render
+    rng = np.random.default_rng(40)
+    n = 200_000
+    t = np.sort(rng.integers(0, 20_000_000, n)).astype(np.int64)
+    x = rng.integers(0, 4, n).astype(np.uint16)
+    y = np.zeros(n, np.uint16)
+    p = rng.choice([-1, 1], n).astype(np.int8)
+    _, Sn, _ = oracle.run(4, 1, (t, x, y, p), [20_000_000], decay_kind=2)
+    _, Se, _ = oracle.run(4, 1, (t, x, y, p), [20_000_000])
+    assert np.abs(Sn).max() > 1.5 and np.abs(Se).max() <= 1.5
+    # the naive state is exactly C * (sum of polarities) per pixel
+    for q in range(4):
+        assert Sn[0, q] == pytest.approx(0.15 * int(p[x == q].astype(np.int64).sum()), abs=1e-9)
+
+
+def test_naive_pure_python_copy_agrees():
+    rng = np.random.default_rng(41)
+    t, x, y, p = _random_stream(rng, 6, 4, 3000, 300_000)
+    tf = np.arange(1, 31) * 10_000
+    f0, S0, T0 = oracle.run(6, 4, (t, x, y, p), tf, s_min=-0.4, s_max=0.5, decay_kind=2)
+    f1, S1, T1 = oracle.py_run(6, 4, (t, x, y, p), tf, s_min=-0.4, s_max=0.5, decay_kind=2)
+    assert np.array_equal(f0, f1) and np.array_equal(T0, T1)
+    assert np.max(np.abs(S0 - S1)) < 1e-12
