@@ -76,6 +76,9 @@ typedef struct {
    *             exponential decay of the camera plugin the paper compares
    *             against (b is ignored).  The device paths
    *             take d = 0 for k dt >= 24 (e^-24 = 3.8e-11).
+   *             2: none -- the naive Eq. 2 integrator S <- S + pC,
+   *             no per-event clamp; frames still clamp (Eq. 13) at render;
+   *             runs on the fp64 kernel (the sum is unbounded).
    * decay_first 0: Alg. 2 order, S <- clamp((S + pC) d);
    *             1: decay, then add, S <- clamp(S d + pC)  (the Eq. 3/5 and
    *             complementary-filter order, reading A1). */

@@ -50,6 +50,7 @@ __device__ __forceinline__ void st_stream4(void* p, uint32_t v) {
 // ~1 ulp relative accuracy near the cutoff (SURVEY 8(c) numerics); dt >= dt_cut
 // (= ceil(1e6/k)) gives d = 0 exactly (reading A14).
 __device__ __forceinline__ float esi_decay(int64_t dt, const DecayParams& dp) {
+  if (dp.bmode == kDecayNone) return 1.f;   // Eq. 2
   if (dt >= dp.dt_cut) return 0.f;
   if (dp.bmode == kDecayExp) {       // exponential variant (A20): exp(-k dt)
     if (dp.use_f64) return (float)exp(-dp.k_us * (double)dt);

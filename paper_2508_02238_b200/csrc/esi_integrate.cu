@@ -50,6 +50,7 @@ struct IntCtx {
 
 // Eq. 4 in fp64 (reading A14: d = 0 exactly from dt_cut = ceil(1e6/k) on)
 __device__ __forceinline__ double wide_decay(int64_t dt, const WideParams& wp) {
+  if (wp.bmode == kDecayNone) return 1.0;   // Eq. 2
   if (dt >= wp.dt_cut) return 0.0;
   if (wp.bmode == kDecayExp) return exp(-wp.k_us * (double)dt);   // exponential variant (A20)
   const double u = 1.0 - wp.k_us * (double)dt;
@@ -233,7 +234,8 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
             const double d = wide_decay(te - c.Tsm[px], a.wp);
             const double s = a.wp.first ? c.Ssm[px] * d + pc          // variant: decay, then add
                                         : (c.Ssm[px] + pc) * d;      // Alg. 2: S <- (S + p C) d(t - T)
-            c.Ssm[px] = fmin(fmax(s, a.wp.smin), a.wp.smax);          // clamp (Eq. 13)
+            c.Ssm[px] = a.wp.bmode == kDecayNone ? s                    // Eq. 2: no clamp
+                                                 : fmin(fmax(s, a.wp.smin), a.wp.smax);   // clamp (Eq. 13)
             c.Tsm[px] = te;                                           // T <- t
             c.tag[px] = 32;
             pend = false;

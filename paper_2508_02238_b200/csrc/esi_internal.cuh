@@ -40,6 +40,8 @@ constexpr int kK2Ctas = ESI_K2_CTAS;
 constexpr unsigned long long kNoError = ~0ull;
 
 constexpr int kDecayExp = 5;   // DecayParams::bmode of the exponential variant (decay_kind 1)
+constexpr int kDecayNone = 6;  // naive Eq. 2 integrator (decay_kind 2): d = 1, no per-event clamp;
+                               // dt_cut = INT64_MAX keeps it on the fp64 wide kernel
 
 struct DecayParams {
   float kh, kl;          // k * 1e-6 split into a float pair (u = 1 - k dt, dt in us)

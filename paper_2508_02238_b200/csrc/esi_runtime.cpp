@@ -251,7 +251,7 @@ int params_ok(const esi_params_t* p) {
   if (!(p->b > 0.0) || !std::isfinite(p->b)) return 0;
   if (!std::isfinite(p->s_min) || !std::isfinite(p->s_max) || !(p->s_min < p->s_max)) return 0;
   if (p->chunk_events < 0) return 0;
-  if (p->decay_kind < 0 || p->decay_kind > 1 || p->decay_first < 0 || p->decay_first > 1) return 0;
+  if (p->decay_kind < 0 || p->decay_kind > 2 || p->decay_first < 0 || p->decay_first > 1) return 0;
   return 1;
 }
 
@@ -262,14 +262,15 @@ void derive_params(esi_handle_t* h) {
   h->dp.kl = (float)(kk - (double)h->dp.kh);
   h->dp.k_us = kk;
   // Eq. 4: d = 0 from dt = 1/k on (A14); exponential variant: d = 0 from k dt = 24 on (A20)
-  const double horizon = (p.decay_kind ? 24.0 : 1.0) * 1e6 / p.k;  // us
-  h->dp.dt_cut = horizon >= 9.0e18 ? INT64_MAX : (int64_t)std::ceil(horizon);
+  const double horizon = (p.decay_kind == 1 ? 24.0 : 1.0) * 1e6 / p.k;  // us
+  h->dp.dt_cut = (horizon >= 9.0e18 || p.decay_kind == 2) ? INT64_MAX : (int64_t)std::ceil(horizon);
   h->dp.use_f64 = h->dp.dt_cut > (int64_t)(1 << 24);
   h->dp.b = (float)p.b;
   h->dp.tau_h = (float)horizon;
   h->dp.tau_l = (float)(horizon - (double)h->dp.tau_h);
   h->dp.kf = (float)kk;
-  h->dp.bmode = p.decay_kind ? kDecayExp : (p.b == 1.0 || p.b == 2.0 || p.b == 3.0 || p.b == 4.0) ? (int)p.b : 0;
+  h->dp.bmode = p.decay_kind == 2 ? kDecayNone
+                : p.decay_kind ? kDecayExp : (p.b == 1.0 || p.b == 2.0 || p.b == 3.0 || p.b == 4.0) ? (int)p.b : 0;
   h->dp.first = p.decay_first ? 1 : 0;
   h->mp.C = (float)p.C;
   h->mp.smin = (float)p.s_min;

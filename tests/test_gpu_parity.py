@@ -437,26 +437,32 @@ def test_pinned_host_pipeline_equals_device_path():
 
 
 # ---------------------------------------------------------------- decay variants
-@pytest.mark.parametrize("kind,first", [(1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("kind,first", [(1, 0), (0, 1), (1, 1), (2, 0)])
 @pytest.mark.parametrize("k", [10.0, 40.0, 0.05])
 @pytest.mark.parametrize("rd", [1, 0])
 def test_decay_variants_against_oracle(kind, first, k, rd):
     """Exponential decay and/or decay-then-add (reading A20) on the fast path
     (k = 10, 40 /s) and the fp64 wide path (k = 0.05 /s: horizon > 2^23 us),
-    with a hot pixel (dense path) and small chunks (state carried across)."""
+    with a hot pixel (dense path) and small chunks (state carried across);
+    kind 2 = the naive Eq. 2 integrator (fp64 kernel, unclamped state)."""
     ev = random_stream(int(100 * kind + 10 * first + k + rd), 40, 30, 60_000, 600_000, hot=0.03)
     prm = dict(DEF, k=k, decay_kind=kind, decay_first=first)
+    if kind == 2:
+        # naive sums sit on the lattice C*n; with C = 0.15 Eq. 14 lands on exact
+        # ties (85 * 0.15 n + 127.5 = X.5) decided by summation rounding, so both
+        # results are correct there; C = 0.125 is exact in binary on both sides
+        prm["C"] = 0.125
     tf = np.arange(1, 61, dtype=np.int64) * 10_000
     check(40, 30, ev, tf, prm, readout_decay=rd, chunk_events=16384)
 
 
-@pytest.mark.parametrize("kind,first", [(1, 0), (1, 1), (0, 1)])
+@pytest.mark.parametrize("kind,first", [(1, 0), (1, 1), (0, 1), (2, 0)])
 def test_decay_variants_readout_only_frames(kind, first):
     """Frames rendered with nothing pending (readout-only kernel) use the same decay."""
     from paper_2508_02238_b200 import Esi
     W, H = 37, 11
     ev = random_stream(5 + kind + first, W, H, 20_000, 200_000)
-    prm = dict(DEF, decay_kind=kind, decay_first=first)
+    prm = dict(DEF, decay_kind=kind, decay_first=first, C=0.125 if kind == 2 else DEF["C"])
     tf1 = np.arange(1, 21, dtype=np.int64) * 10_000
     tf2 = 200_000 + np.arange(1, 11, dtype=np.int64) * 7_000
     f_ref, S_ref, T_ref = oracle_run(W, H, ev, np.concatenate([tf1, tf2]), prm)
@@ -472,7 +478,7 @@ def test_decay_variants_readout_only_frames(kind, first):
 
 def test_decay_variant_params_validated():
     from paper_2508_02238_b200 import Esi, EsiError
-    for bad in (dict(decay_kind=2), dict(decay_first=-1), dict(decay_kind=-1)):
+    for bad in (dict(decay_kind=3), dict(decay_first=-1), dict(decay_kind=-1)):
         with pytest.raises(EsiError) as ei:
             Esi(8, 8, **bad)
         assert ei.value.code == 1
