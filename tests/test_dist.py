@@ -426,3 +426,42 @@ def test_borrowed_buffers_kept_while_pending():
     e.render_many(np.array([100_000], np.int64))
     assert e.pending() == 0 and len(e._borrowed) == 0
     e.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_p2p_router_random_sweep(seed):
+    """Random sensors, band counts (1..64), shard counts and arena fills: the
+    router's count + scatter into per-band arenas equals the stable partition
+    of the whole stream (bit-exact), and bytes outside each run are untouched."""
+    from paper_2508_02238_b200.dist import PeerTransport
+    rng = np.random.default_rng(500 + seed)
+    H = int(rng.integers(1, 300))
+    W = int(rng.integers(1, 500))
+    G = int(rng.integers(1, min(64, H) + 1))
+    S = int(rng.integers(1, 6))
+    n = int(rng.choice([0, 1, 1000, 40_000, 300_000]))
+    a = stream(600 + seed, W, H, n, 2_000_000)
+    starts = row_bands(H, G) if H % G == 0 or -(-H // G) * (G - 1) < H else [round(H * g / G) for g in range(G + 1)]
+    starts = sorted(set(starts))
+    G = len(starts) - 1
+    ev = from_numpy_struct(a).cuda()
+    bounds = time_shard_bounds(len(a), S)
+    T = PeerTransport(0, H, starts)
+    ref, c_ref = np_router(from_numpy_struct(a), starts)
+    pad = [int(rng.integers(0, 9)) for _ in range(G)]
+    bufs = [torch.full((int(c_ref[g]) + pad[g] + 3, 2), -7, dtype=torch.int64, device="cuda") for g in range(G)]
+    torch.cuda.synchronize()
+    M = []
+    for s in range(S):
+        M.append(T.count(ev[bounds[s]:bounds[s + 1]]))
+        off = np.array([pad[g] + sum(int(M[q][g]) for q in range(s)) for g in range(G)], np.int64)
+        T.scatter([b.data_ptr() for b in bufs], off)
+        T.sync()
+    cs = np.concatenate([[0], np.cumsum(c_ref)])
+    for g in range(G):
+        got = bufs[g].cpu()
+        assert torch.equal(got[:pad[g]], torch.full((pad[g], 2), -7, dtype=torch.int64))
+        assert torch.equal(got[pad[g]:pad[g] + int(c_ref[g])], ref[cs[g]:cs[g + 1]]), f"band {g}"
+        assert torch.equal(got[pad[g] + int(c_ref[g]):], torch.full((3, 2), -7, dtype=torch.int64))
+    T.close()
