@@ -211,6 +211,9 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
 
     from paper_2508_02238_b200 import Esi
