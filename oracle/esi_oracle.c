@@ -19,6 +19,7 @@ struct esio {
   int32_t decay_kind;              /* 0: Eq. 4 (ESI); 1: exponential (camera plugin);
                                       2: none -- the naive Eq. 2 integrator, no per-event clamp */
   int32_t decay_first;             /* 0: Alg. 2 order (add, then decay); 1: decay, then add (A1 variant) */
+  int32_t state_unclamped;         /* 1: no per-event Eq. 13 clamp, frames clamp at render */
   double* S;                       /* accumulation matrix */
   int64_t* T;                      /* last decay time matrix */
   int64_t* pt; uint16_t* px; uint16_t* py; int8_t* pp;   /* pending events */
@@ -168,8 +169,14 @@ static void esio_apply_event(esio_t* h, int64_t t, uint16_t x, uint16_t y, int8_
     h->S[i] = h->S[i] + (double)p * h->C;               /* then P:243                     */
   }
   h->T[i] = t;                                          /* P:249  T <- t_i                */
-  if (h->decay_kind != 2)                               /* Eq. 2 has no clamp */
+  if (h->decay_kind != 2 && !h->state_unclamped)        /* Eq. 2 / unclamped variants: no clamp */
     h->S[i] = esio_clamp(h->S[i], h->s_min, h->s_max);  /* P:251  clamp (Eq. 13)          */
+}
+
+int esio_set_unclamped(esio_t* h, int32_t state_unclamped) {
+  if (!h || state_unclamped < 0 || state_unclamped > 1) return ESIO_ERR_INVALID_ARG;
+  h->state_unclamped = state_unclamped;
+  return ESIO_OK;
 }
 
 int esio_set_variant(esio_t* h, int32_t decay_kind, int32_t decay_first) {

@@ -54,6 +54,10 @@ uint8_t esio_map(double v, double s_min, double s_max);
  * still clamp at render);
  * decay_first 0 = Alg. 2 order (add, then decay), 1 = decay, then add. */
 int esio_set_variant(esio_t* h, int32_t decay_kind, int32_t decay_first);
+/* state_unclamped 1: the per-event Eq. 13 clamp is dropped and frames
+ * clamp at render only -- the events-only complementary filter of SPEC
+ * S:243-246, S:266 (with decay_kind 1, decay_first 1). */
+int esio_set_unclamped(esio_t* h, int32_t state_unclamped);
 int esio_create(int32_t width, int32_t height, double C, double k, double b,
                 double s_min, double s_max, int64_t t_origin,
                 int32_t readout_decay, esio_t** out);

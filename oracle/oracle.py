@@ -54,6 +54,7 @@ def lib():
         L.esio_decay.argtypes = [i64, dbl, dbl]; L.esio_decay.restype = dbl
         L.esio_decay_exp.argtypes = [i64, dbl]; L.esio_decay_exp.restype = dbl
         L.esio_set_variant.argtypes = [vp, i32, i32]; L.esio_set_variant.restype = ctypes.c_int
+        L.esio_set_unclamped.argtypes = [vp, i32]; L.esio_set_unclamped.restype = ctypes.c_int
         L.esio_clamp.argtypes = [dbl, dbl, dbl]; L.esio_clamp.restype = dbl
         L.esio_map.argtypes = [dbl, dbl, dbl]; L.esio_map.restype = ctypes.c_uint8
         L.esio_create.argtypes = [i32, i32, dbl, dbl, dbl, dbl, dbl, i64, i32, ctypes.POINTER(vp)]
@@ -111,7 +112,7 @@ class Oracle:
     """Stateful oracle handle (same call structure as the C ABI)."""
 
     def __init__(self, width, height, C=0.15, k=10.0, b=2.0, s_min=-1.5, s_max=1.5,
-                 t_origin=0, readout_decay=1, decay_kind=0, decay_first=0):
+                 t_origin=0, readout_decay=1, decay_kind=0, decay_first=0, state_unclamped=0):
         self.W, self.H = int(width), int(height)
         self.P = self.W * self.H
         h = ctypes.c_void_p()
@@ -121,6 +122,8 @@ class Oracle:
             raise OracleError(rc, "esio_create")
         self._h = h
         rc = lib().esio_set_variant(h, int(decay_kind), int(decay_first))
+        if not rc:
+            rc = lib().esio_set_unclamped(h, int(state_unclamped))
         if rc:
             raise OracleError(rc, "esio_set_variant")
 
@@ -172,11 +175,12 @@ class Oracle:
 
 
 def run(width, height, events, t_frames, C=0.15, k=10.0, b=2.0, s_min=-1.5, s_max=1.5,
-        t_origin=0, readout_decay=1, decay_kind=0, decay_first=0):
+        t_origin=0, readout_decay=1, decay_kind=0, decay_first=0, state_unclamped=0):
     """Whole-stream oracle: returns (frames[F,H,W] u8, S[H,W] f64, T[H,W] i64)."""
-    if decay_kind or decay_first:                 # variants: through the handle
+    if decay_kind or decay_first or state_unclamped:   # variants: through the handle
         o = Oracle(width, height, C=C, k=k, b=b, s_min=s_min, s_max=s_max, t_origin=t_origin,
-                   readout_decay=readout_decay, decay_kind=decay_kind, decay_first=decay_first)
+                   readout_decay=readout_decay, decay_kind=decay_kind, decay_first=decay_first,
+                   state_unclamped=state_unclamped)
         rc = o.push(events)
         if rc:
             raise OracleError(rc, "esio_push")
@@ -217,7 +221,7 @@ def _py_decay(dt_us, k, b, kind=0):
 
 
 def py_run(width, height, events, t_frames, C=0.15, k=10.0, b=2.0, s_min=-1.5, s_max=1.5,
-           t_origin=0, readout_decay=1, decay_kind=0, decay_first=0):
+           t_origin=0, readout_decay=1, decay_kind=0, decay_first=0, state_unclamped=0):
     t, x, y, p = _soa(events)
     S = [0.0] * (width * height)
     T = [int(t_origin)] * (width * height)       # P:239 (A3)
@@ -235,7 +239,7 @@ def py_run(width, height, events, t_frames, C=0.15, k=10.0, b=2.0, s_min=-1.5, s
                 S[q] = S[q] + int(p[i]) * C
                 S[q] = S[q] * _py_decay(dt, k, b, decay_kind)
             T[q] = int(t[i])
-            if decay_kind != 2:                                       # Eq. 2: no clamp
+            if decay_kind != 2 and not state_unclamped:               # Eq. 2 / unclamped: no clamp
                 S[q] = min(max(S[q], s_min), s_max)
             i += 1
         fr = np.empty(width * height, np.uint8)

@@ -544,3 +544,29 @@ def test_naive_pure_python_copy_agrees():
     f1, S1, T1 = oracle.py_run(6, 4, (t, x, y, p), tf, s_min=-0.4, s_max=0.5, decay_kind=2)
     assert np.array_equal(f0, f1) and np.array_equal(T0, T1)
     assert np.max(np.abs(S0 - S1)) < 1e-12
+
+
+def test_complementary_filter_unclamped_state():
+    """Events-only complementary filter: exp decay,
+    decay then add, no per-event clamp, frames clamp at render.  Two +1 events
+    0.2 s apart at alpha = 5 give 0.2052 even with S_max = 0.2; the clamped
+    variant stops at 0.2; the frame is 255 either way; long silence relaxes the
+    frame to the baseline gray."""
+    kw = dict(C=0.15, k=5.0, s_min=-0.2, s_max=0.2, decay_kind=1, decay_first=1)
+    evs = ev([(1_000_000, 0, 0, 1), (1_200_000, 0, 0, 1)])
+    o = Oracle(1, 1, state_unclamped=1, **kw)
+    o.push(evs)
+    assert o.render(1_200_000)[0] == 255
+    assert o.get_state()[0][0, 0] == pytest.approx(0.15 * math.exp(-1.0) + 0.15, rel=1e-14)
+    assert o.render(20_000_000)[0] == 128                       # 18.8 s at alpha = 5: e^-94 -> mid-gray
+    o2 = Oracle(1, 1, **kw)
+    o2.push(evs)
+    o2.flush()
+    assert o2.get_state()[0][0, 0] == 0.2
+    rng = np.random.default_rng(42)
+    t, x, y, p = _random_stream(rng, 6, 4, 3000, 300_000)
+    tf = np.arange(1, 31) * 10_000
+    f0, S0, T0 = oracle.run(6, 4, (t, x, y, p), tf, state_unclamped=1, **kw)
+    f1, S1, T1 = oracle.py_run(6, 4, (t, x, y, p), tf, state_unclamped=1, **kw)
+    assert np.array_equal(f0, f1) and np.max(np.abs(S0 - S1)) < 1e-12
+    assert np.abs(S0).max() > 0.2                                # the state does leave the bounds
