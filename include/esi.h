@@ -84,6 +84,12 @@ typedef struct {
    *             complementary-filter order, reading A1). */
   int32_t decay_kind;
   int32_t decay_first;
+  /* state_unclamped 1: no per-event Eq. 13 clamp; frames still clamp
+   * at render.  With decay_kind 1 and decay_first 1 this is the events-only
+   * complementary filter.  Default 0.  Unclamped
+   * states are unbounded sums that can cancel, so they accumulate in fp64
+   * (the wide kernel; S is stored in fp32 between chunks). */
+  int32_t state_unclamped;
 } esi_params_t;
 
 typedef struct esi_handle esi_handle_t;

@@ -12,7 +12,7 @@ struct FastConst {
   float tau_h, tau_l;                  // tau = 1e6/k us = tau_h + tau_l
   float kh, kl, k_tau_l;               // k_us = kh + kl (no systematic bias), k_us * tau_l
   float b;
-  float C, smin, smax;
+  float C, smin, smax;                 // per-event clamp bounds (+-FLT_MAX when the state is unclamped)
   float scale, off_frac, magic_off;    // map: byte = low8(bits(rd(v*scale + off_frac + 2^23 + off_int)))
   float scale_w2;                      // k_us^2 * scale: Eq. 14 of S*(k w)^2 with k^2 folded in
   int32_t tau_int;                     // tau is an integer (tau_l == 0)
@@ -30,15 +30,15 @@ __device__ __forceinline__ FastConst make_const(const IntArgs& a) {
   c.k_tau_l = a.dp.kf * a.dp.tau_l;
   c.b = a.dp.b;
   c.C = a.mp.C;
-  c.smin = a.mp.smin;
-  c.smax = a.mp.smax;
+  c.smin = a.mp.ev_smin;
+  c.smax = a.mp.ev_smax;
   c.scale = a.mp.scale;
   c.off_frac = a.mp.off_frac;
   c.magic_off = a.mp.magic_off;
   c.scale_w2 = a.mp.scale_w2;
   c.tau_int = a.dp.tau_l == 0.f;
   c.rd = a.mp.readout_decay != 0;
-  c.cl = !(a.mp.smin <= 0.f && a.mp.smax >= 0.f);
+  c.cl = a.mp.readout_clamp;           // bounds exclude 0, or unclamped state: clamp at readout
   c.fold = a.dp.bmode == 2 && c.rd && !c.cl && c.tau_int;   // readout only: independent of the order
   c.dtc = (float)a.dp.dt_cut;          // < 2^23 on the fast path: exact
   return c;
@@ -84,7 +84,8 @@ __device__ __forceinline__ float clampS(float s, const FastConst& c) { return fm
 // = tau - dt (exact), d = (k w)^2 for w > 0 and 0 otherwise, so
 //   x = S w^2 (k^2 scale) + off_frac   -- 4 packed f32x2 ops + 2 max per 2 pixels.
 template <int BM>
-__device__ __forceinline__ uint32_t readout2(float2 s, float2 T, float tj, float aj, const FastConst& c) {
+__device__ __forceinline__ uint32_t readout2(float2 s, float2 T, float tj, float aj, const FastConst& c, float rmin,
+                                             float rmax) {   // rmin, rmax: Eq. 13 bounds of the readout
   float2 x;
   if (c.fold) {
     float2 w = __fadd2_rn(T, make_float2(-aj, -aj));                          // tau - dt, exact
@@ -96,8 +97,8 @@ __device__ __forceinline__ uint32_t readout2(float2 s, float2 T, float tj, float
     float2 v = s;
     if (c.rd) v = __fmul2_rn(s, make_float2(ev_decay<BM>(tj - T.x, c), ev_decay<BM>(tj - T.y, c)));
     if (c.cl) {
-      v.x = fminf(fmaxf(v.x, c.smin), c.smax);
-      v.y = fminf(fmaxf(v.y, c.smin), c.smax);
+      v.x = fminf(fmaxf(v.x, rmin), rmax);
+      v.y = fminf(fmaxf(v.y, rmin), rmax);
     }
     x = __ffma2_rn(v, make_float2(c.scale, c.scale), make_float2(c.off_frac, c.off_frac));
   }

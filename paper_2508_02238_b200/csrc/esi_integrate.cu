@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
             const double d = wide_decay(te - c.Tsm[px], a.wp);
             const double s = a.wp.first ? c.Ssm[px] * d + pc          // variant: decay, then add
                                         : (c.Ssm[px] + pc) * d;      // Alg. 2: S <- (S + p C) d(t - T)
-            c.Ssm[px] = a.wp.bmode == kDecayNone ? s                    // Eq. 2: no clamp
-                                                 : fmin(fmax(s, a.wp.smin), a.wp.smax);   // clamp (Eq. 13)
+            c.Ssm[px] = a.wp.unclamped ? s                              // Eq. 2 / unclamped variants
+                                       : fmin(fmax(s, a.wp.smin), a.wp.smax);   // clamp (Eq. 13)
             c.Tsm[px] = te;                                           // T <- t
             c.tag[px] = 32;
             pend = false;

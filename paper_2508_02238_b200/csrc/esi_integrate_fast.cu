@@ -126,8 +126,8 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
     const int base = q * 4;
     const float4 s0 = *reinterpret_cast<const float4*>(&sm.S[base]);
     const float4 t0 = *reinterpret_cast<const float4*>(&sm.T[base]);
-    const uint32_t b01 = readout2<BM>(make_float2(s0.x, s0.y), make_float2(t0.x, t0.y), tj, aj, c);
-    const uint32_t b23 = readout2<BM>(make_float2(s0.z, s0.w), make_float2(t0.z, t0.w), tj, aj, c);
+    const uint32_t b01 = readout2<BM>(make_float2(s0.x, s0.y), make_float2(t0.x, t0.y), tj, aj, c, a.mp.smin, a.mp.smax);
+    const uint32_t b23 = readout2<BM>(make_float2(s0.z, s0.w), make_float2(t0.z, t0.w), tj, aj, c, a.mp.smin, a.mp.smax);
     const uint32_t v = __byte_perm(b01, b23, 0x5410);
     if (vec && base + 4 <= npx) {
       st_stream4(frame + base, v);

@@ -50,6 +50,7 @@ struct DecayParams {
   int32_t use_f64;
   int32_t bmode;         // 1,2,3,4: integer b fast path; 0: exp2(b log2 u); kDecayExp: exp(-k dt)
   int32_t first;         // 1: decay, then add (variant); 0: Alg. 2 order
+  int32_t unclamped;     // 1: no per-event Eq. 13 clamp (naive Eq. 2, complementary filter)
   float b;
   // fast K2: u = kf * ((tau_h - dt) + tau_l) with tau = 1e6/k us = tau_h + tau_l
   float tau_h, tau_l, kf;
@@ -64,6 +65,8 @@ struct MapParams {
   float scale_w2;        // (k * 1e-6)^2 * scale: folded b = 2 readout of the fast K2
   int32_t off_int;
   float magic_off;       // 2^23 + off_int (exact): RD-add magic of the fast K2 readout
+  float ev_smin, ev_smax; // per-event clamp bounds of the fast K2 (+-FLT_MAX: unclamped state)
+  int32_t readout_clamp;  // the fast K2 readout must clamp (bounds exclude 0, or unclamped state)
   int32_t readout_decay;
 };
 
@@ -74,7 +77,7 @@ struct WideParams {
   double C, k_us, b, smin, smax, scale, off5;
   int64_t dt_cut;
   int32_t bmode, readout_decay;
-  int32_t first;
+  int32_t first, unclamped;
 };
 
 struct PartArgs {

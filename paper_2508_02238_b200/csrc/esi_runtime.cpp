@@ -252,6 +252,7 @@ int params_ok(const esi_params_t* p) {
   if (!std::isfinite(p->s_min) || !std::isfinite(p->s_max) || !(p->s_min < p->s_max)) return 0;
   if (p->chunk_events < 0) return 0;
   if (p->decay_kind < 0 || p->decay_kind > 2 || p->decay_first < 0 || p->decay_first > 1) return 0;
+  if (p->state_unclamped < 0 || p->state_unclamped > 1) return 0;
   return 1;
 }
 
@@ -272,6 +273,11 @@ void derive_params(esi_handle_t* h) {
   h->dp.bmode = p.decay_kind == 2 ? kDecayNone
                 : p.decay_kind ? kDecayExp : (p.b == 1.0 || p.b == 2.0 || p.b == 3.0 || p.b == 4.0) ? (int)p.b : 0;
   h->dp.first = p.decay_first ? 1 : 0;
+  h->dp.unclamped = (p.state_unclamped || p.decay_kind == 2) ? 1 : 0;
+  // finite stand-ins for "no clamp": 0 * bound stays 0 in the dense-path scan
+  h->mp.ev_smin = h->dp.unclamped ? -3.402823466e38f : (float)p.s_min;
+  h->mp.ev_smax = h->dp.unclamped ? 3.402823466e38f : (float)p.s_max;
+  h->mp.readout_clamp = (!(p.s_min <= 0.0 && p.s_max >= 0.0) || h->dp.unclamped) ? 1 : 0;
   h->mp.C = (float)p.C;
   h->mp.smin = (float)p.s_min;
   h->mp.smax = (float)p.s_max;
@@ -293,6 +299,7 @@ void derive_params(esi_handle_t* h) {
   h->wp.dt_cut = h->dp.dt_cut;
   h->wp.bmode = h->dp.bmode;
   h->wp.first = h->dp.first;
+  h->wp.unclamped = h->dp.unclamped;
   h->wp.readout_decay = h->mp.readout_decay;
 }
 
@@ -405,7 +412,9 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   dalloc((void**)&h->d_n_active, sizeof(int32_t));
   if (!rc) rc = ensure_pinned(h, 1 << 16);
   if (!rc) rc = esi_reset(h);
-  h->allow_fast = h->dp.dt_cut < ((int64_t)1 << 23) && !getenv("ESI_DISABLE_FAST");
+  // unclamped states (naive Eq. 2, complementary filter) are unbounded sums that can cancel:
+  // accumulate them in fp64 (wide kernel) rather than fp32
+  h->allow_fast = h->dp.dt_cut < ((int64_t)1 << 23) && !h->dp.unclamped && !getenv("ESI_DISABLE_FAST");
   h->single_stream = getenv("ESI_SINGLE_STREAM") && atoi(getenv("ESI_SINGLE_STREAM")) != 0;
   if (!rc) {
     // K1 rank mode: probe that warp-wide smem atomics serve same-address lanes in lane order

@@ -58,7 +58,7 @@ def test_invalid_arguments_rejected_on_host():
     assert L.esi_create(10, 10, ctypes.byref(bad), ctypes.byref(h)) == 1
     bad = esi.default_params(k=0.0)
     assert L.esi_create(10, 10, ctypes.byref(bad), ctypes.byref(h)) == 1
-    for kw in (dict(decay_kind=3), dict(decay_first=3), dict(decay_kind=-1)):   # kind 0..2, first 0/1
+    for kw in (dict(decay_kind=3), dict(decay_first=3), dict(decay_kind=-1), dict(state_unclamped=2)):
         bad = esi.default_params(**kw)
         assert L.esi_create(10, 10, ctypes.byref(bad), ctypes.byref(h)) == 1
     assert L.esi_strerror(4) == b"negative time interval (events or frames out of order)"

@@ -456,6 +456,18 @@ def test_decay_variants_against_oracle(kind, first, k, rd):
     check(40, 30, ev, tf, prm, readout_decay=rd, chunk_events=16384)
 
 
+@pytest.mark.parametrize("k", [10.0, 40.0, 0.05])
+@pytest.mark.parametrize("rd", [1, 0])
+def test_complementary_filter_against_oracle(k, rd):
+    """Events-only complementary filter (exp decay, decay then add, state
+    unclamped, frames clamped at render) with tight
+    bounds, so the state leaves them."""
+    ev = random_stream(int(7 * k + rd), 40, 30, 60_000, 600_000, hot=0.03)
+    prm = dict(DEF, k=k, s_min=-0.3, s_max=0.3, decay_kind=1, decay_first=1, state_unclamped=1)
+    tf = np.arange(1, 61, dtype=np.int64) * 10_000
+    check(40, 30, ev, tf, prm, readout_decay=rd, chunk_events=16384)
+
+
 @pytest.mark.parametrize("kind,first", [(1, 0), (1, 1), (0, 1), (2, 0)])
 def test_decay_variants_readout_only_frames(kind, first):
     """Frames rendered with nothing pending (readout-only kernel) use the same decay."""
@@ -509,7 +521,8 @@ def _sweep_case(seed):
     kind = int(rng.choice([0, 0, 1]))
     prm = {"C": float(rng.uniform(0.01, 0.5)), "k": float(rng.choice([0.5, 10.0, 100.0, 1000.0])),
            "b": float(rng.choice([0.5, 1.0, 2.0, 3.0, 2.7])), "s_min": lo, "s_max": hi,
-           "decay_kind": kind, "decay_first": int(rng.integers(0, 2))}
+           "decay_kind": kind, "decay_first": int(rng.integers(0, 2)),
+           "state_unclamped": int(rng.random() < 0.2)}
     tf = np.sort(rng.integers(0, span + span // 4, F)).astype(np.int64)
     tf[rng.random(F) < 0.2] = tf[0]                            # duplicated frame times
     tf = np.sort(tf)
@@ -525,7 +538,8 @@ def _boundary_distance(W, H, a, tf, prm, rd):
     cross the boundary (the integer decision is taken on the state)."""
     from helpers import S_ABS, S_REL
     o = oracle.Oracle(W, H, C=prm["C"], k=prm["k"], b=prm["b"], s_min=prm["s_min"], s_max=prm["s_max"],
-                      readout_decay=rd, decay_kind=prm["decay_kind"], decay_first=prm["decay_first"])
+                      readout_decay=rd, decay_kind=prm["decay_kind"], decay_first=prm["decay_first"],
+                      state_unclamped=prm["state_unclamped"])
     o.push(a)
     L = oracle.lib()
     scale = 255.0 / (prm["s_max"] - prm["s_min"])
