@@ -62,3 +62,27 @@ def test_invalid_arguments_rejected_on_host():
         bad = esi.default_params(**kw)
         assert L.esi_create(10, 10, ctypes.byref(bad), ctypes.byref(h)) == 1
     assert L.esi_strerror(4) == b"negative time interval (events or frames out of order)"
+
+
+def test_router_and_ipc_reject_bad_arguments_on_host():
+    """Row-band router / IPC entry points validate their arguments before any
+    CUDA call (so this runs without a GPU)."""
+    from paper_2508_02238_b200 import esi
+    L = esi._lib()
+    r = ctypes.c_void_p()
+    i32 = ctypes.c_int32
+    bad_rows = [((i32 * 3)(0, 5, 9), 10, 2),      # last start != height
+                ((i32 * 3)(1, 5, 10), 10, 2),     # first start != 0
+                ((i32 * 3)(0, 5, 5), 5, 2),       # empty band
+                ((i32 * 2)(0, 10), 10, 0),        # no bands
+                ((i32 * 2)(0, 10), 0, 1)]         # height 0
+    for rows, h, g in bad_rows:
+        assert L.esi_router_create(0, h, rows, g, ctypes.byref(r)) == 1
+    assert L.esi_router_create(0, 10, None, 1, ctypes.byref(r)) == 1
+    assert L.esi_router_count(None, None, 0, None, None) == 1
+    assert L.esi_router_scatter(None, None, None, None) == 1
+    assert L.esi_ipc_get_handle(None, None) == 1
+    assert L.esi_ipc_open(0, None, ctypes.byref(r)) == 1
+    assert L.esi_buffer_alloc(0, 0, ctypes.byref(r)) == 1
+    counts = (ctypes.c_int64 * 2)()
+    assert L.esi_route_bands(0, None, 0, 10, (i32 * 3)(0, 4, 9), 2, None, counts, None) == 1
