@@ -199,10 +199,11 @@ class RowBandSharded:
             self.band.close()
         self.band = None
         self._keep = []
-        if self.p2p is not None:
+        if self.p2p is not None:                             # collective: every rank closes
             for g, d in enumerate(self._dst):
                 if d is not None and g != self.rank:
                     self.p2p.unmap(d)
+            dist.barrier(group=self.group)                   # no peer maps an arena once it is freed
             for a in self._old + ([self._arena] if self._arena is not None else []):
                 self.p2p.free(a)
             self._old, self._arena, self._dst = [], None, [None] * self.world
