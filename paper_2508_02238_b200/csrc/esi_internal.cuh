@@ -20,8 +20,18 @@
 
 namespace esi {
 
-constexpr int kTile = 4096;          // events per partition tile
-constexpr int kPartThreads = 512;    // 16 warps x 8 events per thread
+#ifndef ESI_TILE
+#define ESI_TILE 4096
+#endif
+#ifndef ESI_PART_THREADS
+#define ESI_PART_THREADS 512
+#endif
+#ifndef ESI_PART_CTAS
+#define ESI_PART_CTAS 2
+#endif
+constexpr int kTile = ESI_TILE;                // events per partition tile
+constexpr int kPartThreads = ESI_PART_THREADS; // 16 warps x 8 events per thread
+constexpr int kPartCtas = ESI_PART_CTAS;       // resident K1 CTAs per SM (launch bounds)
 constexpr int kPartWarps = kPartThreads / 32;
 constexpr int kSubBatch = 1024;      // band events staged in smem per sub-batch
 constexpr int kMaxTilesPerChunk = 2048;

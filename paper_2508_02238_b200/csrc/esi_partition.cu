@@ -228,7 +228,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
 }
 
 template <bool RANK_ATOMIC>
-__global__ void __launch_bounds__(kPartThreads, 2) esi_partition_kernel(PartArgs a) {
+__global__ void __launch_bounds__(kPartThreads, kPartCtas) esi_partition_kernel(PartArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   // Chunk entirely after the last frame of this render: nothing to integrate.
   if (a.ev[0].t_us > a.t_cap) return;
