@@ -156,6 +156,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
   const int tid = threadIdx.x;
   const uint32_t tag = gen << 16;
   uint2 evr[kEPT];                                        // this thread's events, kept from claim to apply
+  uint32_t linked = 0;                                    // bit r: event r had a predecessor claim (= next != kEmpty)
 #pragma unroll
   for (int r = 0; r < kEPT; ++r) {                        // claim
     if (e0 + r * kNT >= e1) break;                        // uniform: no thread has an event in this round
@@ -165,7 +166,9 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
       const int px = (int)(evr[r].y & 0x7fffffffu);
       ESI_DCHECK(px < a_bp && i - e0 < kSB);
       const uint32_t old = atomicExch(&sm.head[px], tag | (uint32_t)(i - e0));
-      sm.next[i - e0] = (old & 0xffff0000u) == tag ? (uint16_t)old : (uint16_t)kEmpty;
+      const bool prev = (old & 0xffff0000u) == tag;
+      sm.next[i - e0] = prev ? (uint16_t)old : (uint16_t)kEmpty;
+      linked |= prev ? (1u << r) : 0u;
     }
   }
   __syncthreads();
@@ -180,7 +183,7 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
     if (i < e1) {
       const int px = (int)(evr[r].y & 0x7fffffffu);
       if (sm.head[px] == (tag | me)) {
-        if (sm.next[me] == kEmpty) apply_event<BM>(sm.S, sm.T, px, evr[r], trel, k);
+        if (!((linked >> r) & 1u)) apply_event<BM>(sm.S, sm.T, px, evr[r], trel, k);   // own claim: no reload of next
         else chain = true;
       }
     }
