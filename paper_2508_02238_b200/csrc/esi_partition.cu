@@ -88,12 +88,17 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   const esi_event_t* ev = a.ev + e0;
   const int4* evv = reinterpret_cast<const int4*>(ev);
 
+  // the raw events are read once: evict-first in L2, so that they do not push
+  // out the previous chunk's records that K2 is reading meanwhile
+  uint64_t pol_first;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int i = warp * WEV + r * 32 + lane;
     if (FULL || i < ne) {
       const uint32_t d = (uint32_t)__cvta_generic_to_shared(raw + i);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(evv + i) : "memory");
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(evv + i),
+                   "l"(pol_first) : "memory");
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
