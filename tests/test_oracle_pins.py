@@ -570,3 +570,57 @@ def test_complementary_filter_unclamped_state():
     f1, S1, T1 = oracle.py_run(6, 4, (t, x, y, p), tf, state_unclamped=1, **kw)
     assert np.array_equal(f0, f1) and np.max(np.abs(S0 - S1)) < 1e-12
     assert np.abs(S0).max() > 0.2                                # the state does leave the bounds
+
+
+# ---------------------------------------------------------------- A8: Eq. 14 rounding (SPEC acceptance 9)
+def test_eq14_exact_ties_round_half_away():
+    """Exact ties of the Eq. 14 argument round half away from zero
+    (reading A8).  Hand-rounded values in
+    golden/eq14_ties.json; a half-to-even rounding (rint) fails here."""
+    g = json.load(open(os.path.join(GOLD, "eq14_ties.json")))
+    for c in g["cases"]:
+        assert oracle.map_gray(c["v"], c["lo"], c["hi"]) == c["expect"], c
+
+
+def test_eq14_all_256_gray_levels_randomized_bounds():
+    """SPEC acceptance 9: endpoints map to 0/255, the mid value maps to
+    128, and every target gray level g is reached, exhaustively over all 256
+    levels with randomized bounds.  Bounds are [lo, lo + 255 h] with h a power
+    of two and lo a multiple of h, so v = lo + g h gives the Eq. 14 argument g
+    exactly and v = lo + (g + 1/2) h gives the exact tie g + 1/2, which the
+    stated rule (half away from zero) sends to g + 1."""
+    rng = np.random.default_rng(540)
+    for _ in range(40):
+        h = 2.0 ** int(rng.integers(-10, 5))
+        lo = float(rng.integers(-300, 40)) * h
+        hi = lo + 255.0 * h
+        assert oracle.map_gray(lo, lo, hi) == 0 and oracle.map_gray(hi, lo, hi) == 255
+        assert oracle.map_gray(lo + 127.5 * h, lo, hi) == 128          # mid value (S:184)
+        for gl in range(256):
+            assert oracle.map_gray(lo + gl * h, lo, hi) == gl
+            if gl < 255:
+                assert oracle.map_gray(lo + (gl + 0.5) * h, lo, hi) == gl + 1
+                # just below / above the tie (h/1024, exact) stay on their side
+                below = lo + (gl + 0.5 - 1 / 1024) * h
+                above = lo + (gl + 0.5 + 1 / 1024) * h
+                assert oracle.map_gray(below, lo, hi) == gl
+                assert oracle.map_gray(above, lo, hi) == gl + 1
+        # clamp contracts (S:203-204): idempotent and monotone
+        vs = np.sort(rng.uniform(lo - 10 * h, hi + 10 * h, 64))
+        cl = [oracle.clamp(v, lo, hi) for v in vs]
+        assert all(oracle.clamp(c, lo, hi) == c for c in cl)
+        assert all(a <= b for a, b in zip(cl, cl[1:]))
+        gray = [oracle.map_gray(c, lo, hi) for c in cl]
+        assert all(a <= b for a, b in zip(gray, gray[1:]))
+
+
+def test_eq14_ties_through_the_render_path():
+    """The frame bytes of a render carry the same rounding: state values on
+    exact ties (Alg. 2 literal readout) give the half-away bytes."""
+    g = json.load(open(os.path.join(GOLD, "eq14_ties.json")))
+    for c in g["cases"]:
+        if not (c["lo"] <= 0.0 <= c["hi"]) or c["lo"] == c["hi"]:
+            continue
+        o = Oracle(1, 1, s_min=c["lo"], s_max=c["hi"], readout_decay=0)
+        o.set_state(np.array([c["v"]]), np.array([0]))
+        assert o.render(10)[0, 0] == c["expect"], c
