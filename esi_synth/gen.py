@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Dict, List, Optional
 
@@ -356,20 +357,27 @@ def _c3(device, seed, duration_us=5_000_000):
                     duration_us, "640x480 noise-dominated: BA 2 Hz/px + 10% hot-burst pixels, P(ON)=0.6")
 
 
-def _rotation(W, H, device, seed, duration_us, rate_fn, c=0.15, dt_us=500, name="c4", desc=""):
+def _rotation(W, H, device, seed, duration_us, rate_fn, c=0.15, dt_us=500, name="c4", desc="", sim=None):
+    """Camera roll over a seeded random log texture with a calibrated event rate.
+    On CUDA the threshold-crossing walk runs in the CUDA simulator
+    (esi_synth/csrc/esim.cu); on CPU in torch (``simulate``)."""
     gen = torch.Generator(device=device).manual_seed(seed)
     sc = RotatingTexture(W, H, gen, device)
-    # events per radian: sum_px |dL/dtheta| / c, measured with a finite difference
-    d = 1e-3
-    L0 = sc.L(torch.tensor([0.0], device=device))
-    L1 = sc.L(torch.tensor([d], device=device))
-    ev_per_rad = float((L1 - L0).abs().sum()) / d / c
-    # the reference-level model loses crossings to hysteresis: calibrate the count
-    # per radian with a short count-only run, then scale omega
-    # (steady state only: the first 0.1 rad charges the reference levels up)
-    def count(rad):
-        return simulate(sc.L, lambda ts: ts.astype(np.float64) * 1e-6, 0, int(rad * 1e6), 1000, c, device,
-                        count_only=True)
+    use_cuda = device.type == "cuda" and (sim or os.environ.get("ESI_SYNTH_SIM", "cuda")) == "cuda"
+    if use_cuda:
+        from .cuda_sim import CudaSim, rotation_scene
+        cs = CudaSim(device)
+        scene = rotation_scene(W, H, sc.tex[0, 0].contiguous(), c)
+
+        def count(rad):
+            st = np.arange(0, int(rad * 1e6) + 1, 1000, dtype=np.int64)
+            return int(cs.count(scene, st, (st.astype(np.float64) * 1e-6).astype(np.float32)).sum().item())
+    else:
+        def count(rad):
+            return simulate(sc.L, lambda ts: ts.astype(np.float64) * 1e-6, 0, int(rad * 1e6), 1000, c, device,
+                            count_only=True)
+    # events per radian: calibrated with a short count-only run (steady state only:
+    # the first 0.1 rad charges the reference levels up), then omega is scaled
     ev_per_rad = max(1.0, (count(0.4) - count(0.1)) / 0.3)
     # theta(t) = integral of omega, omega(t) = rate(t) / ev_per_rad
     tt = np.arange(0, duration_us + dt_us, dt_us, dtype=np.int64)
@@ -379,6 +387,12 @@ def _rotation(W, H, device, seed, duration_us, rate_fn, c=0.15, dt_us=500, name=
     def param_of_t(ts):
         return np.interp(ts.astype(np.float64), tt.astype(np.float64), theta)
 
+    if use_cuda:
+        steps = np.arange(0, duration_us + 1, dt_us, dtype=np.int64)
+        if steps[-1] != duration_us:
+            steps = np.append(steps, duration_us)
+        t, x, y, p = cs.simulate(scene, steps, param_of_t(steps).astype(np.float32))
+        return (t, x, y, p), sc
     sig = simulate(sc.L, param_of_t, 0, duration_us, dt_us, c, device, batch=32)
     t, x, y, p = sig
     o = torch.sort(t, stable=True).indices

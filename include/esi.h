@@ -15,15 +15,20 @@
  * Threading: one writer per handle.  All GPU work of a
  * handle runs on its stream (its own, or the one set by esi_set_stream).
  *
- * Errors: every call returns an esi_status (0 = ESI_OK).  Invalid events are
- * detected on the device while they are integrated (fused into the ingest
- * kernel, so no extra pass over the events).  Such an error is STICKY: the
- * render call that found it returns it, the frames and state it produced are
- * unspecified, and every later call returns it until esi_reset().  With
- * params.validate_on_push = 1, esi_push_events instead validates the batch
- * eagerly (one extra read of the batch) and rejects it atomically: on error
- * none of its events is kept and the handle stays usable.  CUDA failures
- * latch ESI_ERR_CUDA (sticky, also cleared only by esi_reset).
+ * Errors: every call returns an esi_status (0 = ESI_OK).  By default
+ * (params.validate_on_push = 1) esi_push_events validates the batch on the
+ * device before it returns (SURVEY 8(b) "atomic push"): on an
+ * invalid event it returns the error, keeps none of the batch's events and
+ * the handle stays usable -- a rejected push therefore never reaches a render,
+ * which writes no frame and leaves S and T untouched.  This costs one extra
+ * device read of each pushed batch.
+ * With params.validate_on_push = 0 ("fused" mode, for trusted streams) the
+ * checks run inside the ingest kernel during the render instead (no extra
+ * pass).  An invalid event found there is STICKY: the render returns it,
+ * S and T are restored to their value at the start of that render (nothing
+ * is integrated), the frames it wrote are unspecified, and every later call
+ * returns the error until esi_reset().  (reading A21.)
+ * CUDA failures latch ESI_ERR_CUDA (sticky, also cleared only by esi_reset).
  */
 #ifndef ESI_H
 #define ESI_H
@@ -69,7 +74,7 @@ typedef struct {
   int32_t readout_decay; /* 1: frame value S*d(t_frame - T), non-mutating (reading A4);
                             0: Alg. 2 literal, frame maps the stored S             */
   int32_t device;        /* CUDA device ordinal                                            */
-  int32_t validate_on_push; /* 1: eager, atomic validation in esi_push_events (see above) */
+  int32_t validate_on_push; /* 1 (default): atomic validation in esi_push_events; 0: fused (see above) */
   int32_t chunk_events;  /* events per pipeline chunk; 0 = default (8 Mi)                  */
   /* Decay variants (reading A20), default 0 = ESI:
    * decay_kind  0: Eq. 4 d = max{(1 - k dt)^b, 0};  1: d = exp(-k dt), the
@@ -95,11 +100,14 @@ typedef struct {
 typedef struct esi_handle esi_handle_t;
 
 /* Fills *p with the defaults: C=0.15, k=10, b=2, s_min=-1.5, s_max=1.5 (SPEC S:134,
- * S:210-211), t_origin 0, readout_decay 1, device 0, lazy validation. */
+ * S:210-211), t_origin 0, readout_decay 1, device 0, validate_on_push 1 (atomic). */
 void esi_default_params(esi_params_t* p);
 
 /* Creates a handle for a width x height sensor (1 <= width, height <= 65535,
- * width*height <= 2^22 = 4194304).  Allocates the per-pixel state S (fp32) and T (int64)
+ * width*height <= 2^22 = 4194304 pixels: 1024 bands of <= 4096 pixels, the
+ * shared-memory band state of the integrate kernel; the largest BASELINE
+ * sensor, 2560x1440, is 3.7 Mpx.  Larger sensors are split into row bands
+ * across handles / GPUs, esi_route_bands; reading A22).  Allocates the per-pixel state S (fp32) and T (int64)
  * on the device, S = 0, T = t_origin (Alg. 2 "Initialize").
  * Returns ESI_ERR_INVALID_ARG for bad sizes/params, ESI_ERR_OOM, ESI_ERR_CUDA. */
 int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_handle_t** out);
@@ -219,13 +227,17 @@ int esi_stream_sync(int32_t device, void* stream);
 
 /* Per-kernel device time accumulated by the handle when timing is enabled
  * (cudaEvents around each launch, on the handle's stream).  kind:
- * 0 = ingest/partition, 1 = integrate+readout, 2 = readout-only, 3 = other. */
+ * 0 = ingest/partition, 1 = integrate+readout, 2 = readout-only, 3 = push validation. */
 int esi_enable_kernel_timing(esi_handle_t* h, int enable);
 int esi_kernel_time(esi_handle_t* h, int kind, double* ms_total, int64_t* launches);
 /* Counters of the last render call: launches of this library's kernels,
  * events integrated, chunks. */
 int esi_last_render_stats(esi_handle_t* h, int64_t* kernel_launches, int64_t* events,
                           int64_t* chunks);
+
+/* The handle's band layout: bands (K1 partition buckets = integrate CTAs),
+ * pixels per band, warps per integrate CTA.  Any pointer may be NULL. */
+int esi_layout(esi_handle_t* h, int32_t* n_bands, int32_t* band_px, int32_t* warps_per_band);
 
 /* Debug export of the bit-exact grouping step: runs only the
  * ingest/partition kernel over the pending events of the first chunk and

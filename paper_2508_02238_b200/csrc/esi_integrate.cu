@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
   const int64_t px0 = (int64_t)band * a.band_px;            // band_px <= BP
   const int npx = (int)min((int64_t)a.band_px, a.P - px0);
 
+  if (a.gate && *a.gate != kNoError) return;   // lazy validation found an invalid event: write nothing
   const ChunkInfo ci = *a.info;
   const int f_lo = ci.f_lo, f_hi = ci.f_hi;
   const bool active = ci.active != 0;
@@ -276,12 +277,14 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
 template <int NW>
 static cudaError_t launch_nw(const IntArgs& a, cudaStream_t s) {
   const size_t smem = integrate_smem_bytes(NW * kWarpPx);
-  static bool configured = false;
-  if (!configured) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int configured[64] = {0};   // per device (the attribute is per context)
+  if (dev < 0 || dev >= 64 || !configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(esi_integrate_wide_kernel<NW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    if (dev >= 0 && dev < 64) configured[dev] = 1;
   }
   esi_integrate_wide_kernel<NW><<<a.nb, NW * 32, smem, s>>>(a);
   return cudaGetLastError();

@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
   const int n_tiles = a.n_tiles;
   const FastSmem sm = carve(smem_raw, bp, n_tiles);
 
+  if (a.gate && *a.gate != kNoError) return;   // lazy validation found an invalid event: write nothing
   const ChunkInfo ci = *a.info;
   const int f_lo = ci.f_lo, f_hi = ci.f_hi;
   const bool active = ci.active != 0;
@@ -430,13 +431,15 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
 template <int BM>
 cudaError_t launch_fast_b(const IntArgs& a, cudaStream_t s) {
   const size_t smem = fast_smem_bytes(a.band_px, a.n_tiles);
-  static size_t configured = 0;
-  if (smem > configured) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int configured[64] = {0};   // per device (the attribute is per context)
+  if (dev < 0 || dev >= 64 || !configured[dev]) {
     const size_t mx = fast_smem_bytes(kMaxBandPx, kMaxTilesPerChunk);
     cudaError_t e = cudaFuncSetAttribute(esi_integrate_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)mx);
     if (e != cudaSuccess) return e;
-    configured = mx;
+    if (dev >= 0 && dev < 64) configured[dev] = 1;
   }
   esi_integrate_kernel<BM><<<a.nb, kNT, smem, s>>>(a);
   return cudaGetLastError();

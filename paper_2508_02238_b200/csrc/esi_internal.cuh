@@ -142,6 +142,11 @@ struct IntArgs {
   DecayParams dp;
   MapParams mp;
   WideParams wp;
+  // warp-owned K2 (esi_integrate_warp.cu): warps per CTA, quads per warp,
+  // (q * w2_qmagic) >> 32 == q / w2_qpw, events per sub-batch
+  int32_t w2_nw, w2_qpw, w2_sb;
+  uint32_t w2_qmagic;
+  const unsigned long long* gate;    // non-null: exit without writing if *gate != kNoError
 };
 
 struct ReadoutArgs {
@@ -174,6 +179,9 @@ cudaError_t launch_plan(const esi_event_t* const* chunk_first, const int64_t* ch
                         int32_t* n_active, cudaStream_t s);
 // fast kernel (32-bit relative times, dt_cut < 2^23) -- esi_integrate_fast.cu
 cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s);
+// warp-owned fast kernel (32-bit relative times, dt_cut < 2^23) -- esi_integrate_warp.cu
+cudaError_t launch_integrate_w2(const IntArgs& a, cudaStream_t s);
+size_t integrate_w2_smem_bytes(int band_px, int sb, int n_tiles);
 // consume: for segment k, count events with t <= t_cap (binary search), and set
 // *last_t to the t of the last consumed event of the last segment with one.
 cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,

@@ -246,12 +246,14 @@ __global__ void __launch_bounds__(kPartThreads, kPartCtas) esi_partition_kernel(
 template <bool RA>
 static cudaError_t launch_part_t(const PartArgs& a, int n_tiles, cudaStream_t s) {
   const size_t smem = partition_smem_bytes(a.nb);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel<RA>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int configured[64] = {0};   // per device (the attribute is per context); the maximum once
+  if (dev < 0 || dev >= 64 || !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel<RA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)partition_smem_bytes(kMaxBands));
     if (e != cudaSuccess) return e;
-    configured = smem;
+    if (dev >= 0 && dev < 64) configured[dev] = 1;
   }
   esi_partition_kernel<RA><<<n_tiles, kPartThreads, smem, s>>>(a);
   return cudaGetLastError();

@@ -58,6 +58,8 @@ struct esi_handle {
   cudaStream_t own_stream = nullptr, stream = nullptr;
   float* dS = nullptr;
   int64_t* dT = nullptr;
+  float* dS_snap = nullptr;      // lazy-validation mode: state at the start of the render, restored
+  int64_t* dT_snap = nullptr;    // if the render finds an invalid event (S and T stay untouched)
   std::vector<Segment> segs;
   // K1/K2 scratch, double-buffered: K1 of chunk c+1 (stream aux) overlaps K2 of chunk c
   uint2* rec[2] = {nullptr, nullptr};
@@ -106,6 +108,10 @@ struct esi_handle {
   bool atomic_rank = true;   // K1 ranks from lane-ordered smem atomics (probed at create)
   bool allow_fast = true;    // K2 fast variant allowed (dt_cut < 2^23)
   bool single_stream = false; // ESI_SINGLE_STREAM=1: K1 and K2 on one stream
+  bool k2_warp = true;        // K2 = warp-owned kernel (esi_integrate_warp.cu); ESI_K2=block: the older
+                              // block-synchronous kernel (esi_integrate_fast.cu), kept for A/B measurements
+  int w2_nw = 1, w2_qpw = 64, w2_sb = 2048;
+  uint32_t w2_qmagic = 0;
 };
 
 namespace {
@@ -318,7 +324,7 @@ void esi_default_params(esi_params_t* p) {
   p->t_origin_us = 0;
   p->readout_decay = 1;
   p->device = 0;
-  p->validate_on_push = 0;
+  p->validate_on_push = 1;   // atomic push; 0 = fused lazy validation
   p->chunk_events = 0;
 }
 
@@ -357,23 +363,51 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   h->P = P;
   h->prm = prm;
   derive_params(h);
-  // Band size (K1 partition key, K2 CTA): a multiple of 64 pixels such that
-  // the bands fill the SMs evenly at kK2Ctas resident K2 CTAs (8 warps each) per SM
-  // (c4, 4 per SM: 576 bands of 1600 pixels on 148 SMs), at most kMaxBandPx (shared memory) and at most
-  // kMaxBands bands (K1's shared-memory histograms).
+  // Band size (K1 partition key, K2 CTA).
+  //  * warp-owned K2 (default): 2 CTAs per SM; band_px = ceil(P / (2 * #SMs)) rounded up
+  //    to whole quads (4 px), 128 <= band_px <= kMaxBandPx, <= kMaxBands bands;
+  //    nw = ceil(quads / 64) warps of qpw = ceil(quads / nw) <= 64 quads each (two readout
+  //    steps of 32 lanes x 4 px per warp and frame).  c4: 296 bands of 3116 px, 13 warps.
+  //  * block-synchronous K2 (ESI_K2=block): a multiple of 64 pixels such that the bands fill
+  //    the SMs evenly at kK2Ctas resident 8-warp CTAs per SM (c4: 437 bands of 2112 px).
   {
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, prm.device);
-    const int64_t slots = (int64_t)n_sm * kK2Ctas;
-    int64_t bp = (P + slots - 1) / slots;
-    bp = ((bp + 63) / 64) * 64;
-    bp = std::max<int64_t>(64, std::min<int64_t>(bp, kMaxBandPx));
-    while ((P + bp - 1) / bp > kMaxBands) bp += 64;
+    const char* k2e = getenv("ESI_K2");
+    h->k2_warp = !(k2e && strcmp(k2e, "block") == 0);
+    int64_t bp;
+    if (h->k2_warp) {
+      int ctas = 2;
+      if (const char* e = getenv("ESI_K2_CTAS")) ctas = std::max(1, std::min(4, atoi(e)));
+      const int64_t slots = (int64_t)n_sm * ctas;
+      bp = (P + slots - 1) / slots;
+      bp = ((bp + 3) / 4) * 4;
+      bp = std::max<int64_t>(128, std::min<int64_t>(bp, kMaxBandPx));
+      while ((P + bp - 1) / bp > kMaxBands) bp += 4;
+    } else {
+      const int64_t slots = (int64_t)n_sm * kK2Ctas;
+      bp = (P + slots - 1) / slots;
+      bp = ((bp + 63) / 64) * 64;
+      bp = std::max<int64_t>(64, std::min<int64_t>(bp, kMaxBandPx));
+      while ((P + bp - 1) / bp > kMaxBands) bp += 64;
+    }
     if (const char* e = getenv("ESI_BAND_PX")) {
       const int64_t v = atoll(e);
-      if (v >= 64 && v <= kMaxBandPx && v % 64 == 0 && (P + v - 1) / v <= kMaxBands) bp = v;
+      const int64_t mult = h->k2_warp ? 4 : 64;
+      if (v >= 64 && v <= kMaxBandPx && v % mult == 0 && (P + v - 1) / v <= kMaxBands) bp = v;
     }
     h->band_px = (int)bp;
+    const int quads = (int)((bp + 3) / 4);
+    h->w2_nw = (quads + 63) / 64;
+    h->w2_qpw = (quads + h->w2_nw - 1) / h->w2_nw;
+    h->w2_qmagic = (uint32_t)((((uint64_t)1) << 32) / (uint64_t)h->w2_qpw + 1);
+    for (uint32_t q = 0; q < 1024; ++q)   // exactness of the owner division (checked once)
+      if ((uint32_t)(((uint64_t)q * h->w2_qmagic) >> 32) != q / (uint32_t)h->w2_qpw) { delete h; return ESI_ERR_INVALID_ARG; }
+    h->w2_sb = 2048;
+    if (const char* e = getenv("ESI_K2_SB")) {
+      const int v = atoi(e);
+      if (v >= 256 && v <= 2048 && v % 32 == 0) h->w2_sb = v;
+    }
   }
   h->nb = (int)((P + h->band_px - 1) / h->band_px);
   h->band_magic = ((uint64_t)1 << 40) / (uint64_t)h->band_px + 1;   // exact pid / band_px for pid < 2^23
@@ -454,7 +488,8 @@ void esi_destroy(esi_handle_t* h) {
   if (h->aux) cudaStreamSynchronize(h->aux);
   void* bufs[] = {h->dS, h->dT, h->rec[0], h->meta[0], h->tile_t0[0], h->tile_wide[0], h->wide_t[0],
                   h->rec[1], h->meta[1], h->tile_t0[1], h->tile_wide[1], h->wide_t[1], h->d_tf,
-                  (void*)h->d_chunk_first, h->d_chunk_n, h->d_info, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames};
+                  (void*)h->d_chunk_first, h->d_chunk_n, h->d_info, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames,
+                  h->dS_snap, h->dT_snap};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int b = 0; b < 2; ++b) {
@@ -538,9 +573,12 @@ int esi_push_events(esi_handle_t* h, const esi_event_t* events, size_t n) {
   if (h->prm.validate_on_push) {
     const int64_t* prev = h->segs.empty() ? h->d_last_t : &h->segs.back().ptr[h->segs.back().n - 1].t_us;
     ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), h->stream));
+    TimedLaunch tl;
+    timed_begin(h, 3, &tl);
     ESI_CUDA(h, launch_validate(sg.ptr, sg.n, prev, h->prm.t_origin_us,
                                 h->has_last_frame ? h->last_frame_t : INT64_MIN, h->W, h->H, h->d_err,
                                 h->stream));
+    timed_end(h, &tl);
     unsigned long long* herr = (unsigned long long*)h->h_pin;
     ESI_CUDA(h, cudaMemcpyAsync(herr, h->d_err, sizeof(*herr), cudaMemcpyDeviceToHost, h->stream));
     ESI_CUDA(h, cudaStreamSynchronize(h->stream));
@@ -659,6 +697,18 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     ESI_CUDA(h, cudaStreamSynchronize(st));
     const int n_act = std::max(1, *hna);
     ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
+    const bool lazy = !h->prm.validate_on_push;
+    if (lazy) {   // lazy validation (fused in K1): keep the state so that a failing render leaves it untouched
+      if (!h->dS_snap) {
+        if (cudaMalloc((void**)&h->dS_snap, h->P * sizeof(float)) != cudaSuccess ||
+            cudaMalloc((void**)&h->dT_snap, h->P * sizeof(int64_t)) != cudaSuccess) {
+          cudaGetLastError();
+          return ESI_ERR_OOM;
+        }
+      }
+      ESI_CUDA(h, cudaMemcpyAsync(h->dS_snap, h->dS, h->P * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      ESI_CUDA(h, cudaMemcpyAsync(h->dT_snap, h->dT, h->P * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
 
     // K1 runs on the aux stream, K2 on the handle's stream; chunk c uses buffer c & 1:
     // K1(c) waits for the render's setup and for K2(c-2); K2(c) waits for K1(c).
@@ -731,10 +781,15 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       ia.dp = h->dp;
       ia.mp = h->mp;
       ia.wp = h->wp;
+      ia.w2_nw = h->w2_nw;
+      ia.w2_qpw = h->w2_qpw;
+      ia.w2_sb = h->w2_sb;
+      ia.w2_qmagic = h->w2_qmagic;
+      ia.gate = lazy ? h->d_err : nullptr;   // a K1 error so far: K2 exits (frames unspecified, S/T restored)
       TimedLaunch t2;
       timed_begin(h, 1, &t2);
       if (hinfo[c].fast) {
-        ESI_CUDA(h, launch_integrate_fast(ia, st));
+        ESI_CUDA(h, h->k2_warp ? launch_integrate_w2(ia, st) : launch_integrate_fast(ia, st));
         h->st_fast += 1;
       } else {
         ESI_CUDA(h, launch_integrate(ia, st));
@@ -764,7 +819,18 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     ESI_CUDA(h, cudaMemcpyAsync(hcons, h->d_cons, (last_seg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     ESI_CUDA(h, cudaMemcpyAsync(herr, h->d_err, sizeof(*herr), cudaMemcpyDeviceToHost, st));
     ESI_CUDA(h, cudaStreamSynchronize(st));
-    if (*herr != kNoError) h->sticky = (int)(*herr & 0xff);
+    if (*herr != kNoError) {
+      h->sticky = (int)(*herr & 0xff);
+      if (lazy) {   // restore the state of the render's start; nothing is consumed
+        cudaMemcpyAsync(h->dS, h->dS_snap, h->P * sizeof(float), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(h->dT, h->dT_snap, h->P * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+        if (stream_frames) cudaStreamSynchronize(h->d2h);
+        cudaStreamSynchronize(st);
+        cudaGetLastError();
+        collect_timing(h);
+        return h->sticky;
+      }
+    }
     std::vector<Segment> keep;
     for (int k = 0; k < (int)h->segs.size(); ++k) {
       Segment s = h->segs[k];
@@ -823,6 +889,14 @@ int esi_kernel_time(esi_handle_t* h, int kind, double* ms_total, int64_t* launch
   if (!h || kind < 0 || kind > 3) return ESI_ERR_INVALID_ARG;
   if (ms_total) *ms_total = h->kt_ms[kind];
   if (launches) *launches = h->kt_n[kind];
+  return ESI_OK;
+}
+
+int esi_layout(esi_handle_t* h, int32_t* n_bands, int32_t* band_px, int32_t* warps_per_band) {
+  if (!h) return ESI_ERR_INVALID_ARG;
+  if (n_bands) *n_bands = h->nb;
+  if (band_px) *band_px = h->band_px;
+  if (warps_per_band) *warps_per_band = h->k2_warp ? h->w2_nw : 8;
   return ESI_OK;
 }
 

@@ -181,6 +181,11 @@ class RowBandSharded:
             from .esi import Esi
             band_factory = lambda w, h, **p: Esi(w, h, **p)   # noqa: E731
         self.band = band_factory(self.W, self.rows, **params)
+        # The band handle works on torch's current stream: the NCCL exchange output it
+        # borrows zero-copy and the frame buffer zero-fill are ordered on that stream,
+        # so the handle's kernels must be too (a private stream would race with both).
+        if self.device.type == "cuda" and hasattr(self.band, "set_stream"):
+            self.band.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
         self.p2p = transport
         if transport is None:
             self.router = router if router is not None else device_router(self.device.index or 0, self.H)
@@ -279,23 +284,57 @@ class RowBandSharded:
         return rc
 
     # -- rendering + assembly -----------------------------------------------
-    def render_many(self, t_frames, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    ASSEMBLY_BATCH = 64                                     # frames per coalesced (grouped) all-gather
+
+    def _assemble(self, band: torch.Tensor, buf: torch.Tensor):
+        """Frame assembly: all_gather_into_tensor of every frame's band slice into
+        frame j of buf (rank-major = row-major, so each frame lands in place).
+        On NCCL, batches of frames are issued as one coalesced group
+        (ncclGroupStart/End of the per-frame all-gathers: one launch per batch)."""
+        F = band.shape[0]
+        coalesce = dist.get_backend(self.group) == "nccl"
+        for j0 in range(0, F, self.ASSEMBLY_BATCH):
+            j1 = min(F, j0 + self.ASSEMBLY_BATCH)
+            if coalesce:
+                from torch.distributed.distributed_c10d import _coalescing_manager
+                with _coalescing_manager(group=self.group, device=self.device, async_ops=True) as cm:
+                    for j in range(j0, j1):
+                        dist.all_gather_into_tensor(buf[j].view(-1), band[j].view(-1), group=self.group)
+                cm.wait()
+            else:
+                for j in range(j0, j1):
+                    dist.all_gather_into_tensor(buf[j].view(-1), band[j].view(-1), group=self.group)
+
+    def render_many(self, t_frames, out: Optional[torch.Tensor] = None, stage_ms: Optional[dict] = None) -> torch.Tensor:
         """Renders this rank's band for every frame time and assembles the full
-        [F, H, W] frames on every rank (all_gather over the group)."""
+        [F, H, W] frames on every rank (all_gather over the group).  stage_ms:
+        if given, the band render and the assembly are timed separately (CUDA
+        events on the current stream) and accumulated into it."""
         tf = np.ascontiguousarray(t_frames, dtype=np.int64)
         F = len(tf)
-        band = torch.zeros((F, self.bh, self.W), dtype=torch.uint8, device=self.device)
+        timing = stage_ms is not None and self.device.type == "cuda"
+        if timing:
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+        band = torch.empty((F, self.bh, self.W), dtype=torch.uint8, device=self.device)
         if self.rows == self.bh:
             self.band.render_many(tf, band)
         else:                                                # short last band: render, then pad
+            band[:, self.rows:].zero_()
             part = torch.empty((F, self.rows, self.W), dtype=torch.uint8, device=self.device)
             self.band.render_many(tf, part)
             band[:, :self.rows].copy_(part)
+        if timing:
+            e1.record()
         full_h = self.bh * self.world
         direct = out is not None and full_h == self.H and out.is_contiguous()
         buf = out if direct else torch.empty((F, full_h, self.W), dtype=torch.uint8, device=self.device)
-        for j in range(F):                                   # frame j: rank-major = row-major
-            dist.all_gather_into_tensor(buf[j].view(-1), band[j].view(-1), group=self.group)
+        self._assemble(band, buf)
+        if timing:
+            e2.record()
+            e2.synchronize()
+            stage_ms["band_render"] = stage_ms.get("band_render", 0.0) + e0.elapsed_time(e1)
+            stage_ms["assembly"] = stage_ms.get("assembly", 0.0) + e1.elapsed_time(e2)
         self._keep = []
         if self.p2p is not None:
             self._recycle_arenas()

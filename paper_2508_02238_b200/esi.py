@@ -79,6 +79,7 @@ def _lib():
         L.esi_enable_kernel_timing.argtypes = [vp, ctypes.c_int]
         L.esi_kernel_time.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.esi_last_render_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.esi_layout.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
         L.esi_debug_partition.argtypes = [vp, vp, vp, vp, sz, vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
         L.esi_router_create.argtypes = [i32, i32, vp, i32, ctypes.POINTER(vp)]
         L.esi_router_count.argtypes = [vp, vp, sz, vp, vp]
@@ -98,7 +99,7 @@ def _lib():
         for f in ("esi_create", "esi_push_events", "esi_render", "esi_render_many", "esi_get_state",
                   "esi_set_state", "esi_reset", "esi_set_stream", "esi_get_error",
                   "esi_enable_kernel_timing", "esi_kernel_time", "esi_last_render_stats",
-                  "esi_debug_partition"):
+                  "esi_debug_partition", "esi_layout"):
             getattr(L, f).restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -292,6 +293,12 @@ class Esi:
         _check(_lib().esi_last_render_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
                "esi_last_render_stats")
         return {"kernel_launches": a.value, "events": b.value, "chunks": c.value}
+
+    def layout(self):
+        """(bands, pixels per band, warps per integrate CTA) of this handle."""
+        a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(_lib().esi_layout(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "esi_layout")
+        return a.value, b.value, c.value
 
     def debug_partition(self, n_max: int):
         t = np.empty(n_max, np.int64)

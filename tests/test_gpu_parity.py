@@ -261,9 +261,9 @@ def test_errors_are_reported():
                        ([(5, 0, 6, 1)], esi.ESI_ERR_OUT_OF_BOUNDS),
                        ([(5, 1, 1, 0)], esi.ESI_ERR_BAD_POLARITY),
                        ([(5, 1, 1, 1), (4, 1, 1, 1)], esi.ESI_ERR_NEGATIVE_INTERVAL)]:
-        e = Esi(W, H)
+        e = Esi(W, H, validate_on_push=0)
         try:
-            assert e.push(from_numpy_struct(mk_events(rows)).cuda()) == 0   # lazy validation
+            assert e.push(from_numpy_struct(mk_events(rows)).cuda()) == 0   # fused (lazy) validation
             out = torch.empty((1, H, W), dtype=torch.uint8, device="cuda")
             assert e.render_many_rc([100], out) == code
             assert e.error() == code                                       # sticky
@@ -271,7 +271,7 @@ def test_errors_are_reported():
             assert e.error() == 0
         finally:
             e.close()
-        e = Esi(W, H, validate_on_push=1)                                  # eager, atomic
+        e = Esi(W, H)                                                      # default: atomic push
         try:
             assert e.push(from_numpy_struct(mk_events(rows)).cuda()) == code
             assert e.error() == 0
@@ -280,14 +280,20 @@ def test_errors_are_reported():
         finally:
             e.close()
     # first error in stream order wins, as in the oracle
-    e = Esi(W, H)
+    e = Esi(W, H, validate_on_push=0)
     try:
         e.push(from_numpy_struct(mk_events([(1, 1, 1, 1), (2, 1, 1, 5), (3, 9, 9, 1)])).cuda())
         assert e.render_many_rc([10], np.empty((1, H, W), np.uint8)) == esi.ESI_ERR_BAD_POLARITY
     finally:
         e.close()
-    # events not later than the last rendered frame, frames going back in time
     e = Esi(W, H)
+    try:
+        assert e.push(from_numpy_struct(mk_events([(1, 1, 1, 1), (2, 1, 1, 5), (3, 9, 9, 1)])).cuda()) == \
+            esi.ESI_ERR_BAD_POLARITY
+    finally:
+        e.close()
+    # events not later than the last rendered frame, frames going back in time
+    e = Esi(W, H, validate_on_push=0)
     try:
         e.push(from_numpy_struct(mk_events([(1, 1, 1, 1)])).cuda())
         e.render_many([10])
@@ -329,6 +335,69 @@ def sparse_window_stream(seed, W, H, F, per_window, period=10_000):
             rows.append((int(t), int(q % W), int(q // W), int(rng.choice([-1, 1]))))
     rows.sort(key=lambda r: r[0])
     return mk_events(rows)
+
+
+@pytest.mark.parametrize("host_out", [False, True])
+def test_rejected_push_or_render_leaves_state_and_frames_untouched(host_out):
+    """SURVEY 8(b) atomic push: a rejected push integrates nothing and the
+    render that follows writes exactly the frames of the accepted events; a
+    rejected render (frame time going back) writes no byte of `out` and leaves
+    S and T byte-identical.  Fused mode (validate_on_push = 0, reading A21):
+    a render that meets an invalid event leaves S and T byte-identical."""
+    from paper_2508_02238_b200 import Esi, esi
+    w = wl("c2", duration_us=300_000)
+    W, H = w.W, w.H
+    ev = to_numpy_struct(w.events)
+    cut = int(np.searchsorted(ev["t"], 100_000, side="right"))
+    first = from_numpy_struct(ev[:cut]).cuda()
+    bad = mk_events([(150_000, 3, 3, 1), (150_001, W, 0, 1)])      # second event out of bounds
+    rest = from_numpy_struct(ev[cut:]).cuda()
+
+    def new_out(n):
+        if host_out:
+            return np.full((n, H, W), 0x5A, np.uint8)
+        return torch.full((n, H, W), 0x5A, dtype=torch.uint8, device="cuda")
+
+    e = Esi(W, H, **w.params)
+    try:
+        assert e.push(first) == 0
+        f0 = new_out(10)
+        e.render_many(np.arange(1, 11) * 10_000, f0)
+        S0, T0 = e.get_state()
+        # rejected push: nothing kept
+        assert e.push(from_numpy_struct(bad).cuda()) == esi.ESI_ERR_OUT_OF_BOUNDS
+        assert e.pending() == 0 and e.error() == 0
+        S1, T1 = e.get_state()
+        assert S1.tobytes() == S0.tobytes() and T1.tobytes() == T0.tobytes()
+        # rejected render: out untouched, state untouched
+        o = new_out(2)
+        assert e.render_many_rc([90_000, 95_000], o) == esi.ESI_ERR_NEGATIVE_INTERVAL
+        o_np = o.cpu().numpy() if hasattr(o, "cpu") else o
+        assert (o_np == 0x5A).all()
+        S2, T2 = e.get_state()
+        assert S2.tobytes() == S0.tobytes() and T2.tobytes() == T0.tobytes()
+        # the stream goes on as if the bad push never happened
+        assert e.push(rest) == 0
+        f1 = e.render_many(np.arange(11, 31) * 10_000)
+    finally:
+        e.close()
+    f_ref, S_ref, T_ref = oracle_run(W, H, ev, np.arange(1, 31) * 10_000, w.params)
+    f0_np = f0.cpu().numpy() if hasattr(f0, "cpu") else f0
+    assert_frames_close(np.concatenate([f0_np, f1]), f_ref)
+
+    # fused mode: the failing render restores S and T
+    e = Esi(W, H, validate_on_push=0, **w.params)
+    try:
+        assert e.push(first) == 0
+        e.render_many(np.arange(1, 11) * 10_000)
+        S0, T0 = e.get_state()
+        assert e.push(from_numpy_struct(bad).cuda()) == 0              # accepted lazily
+        assert e.render_many_rc([200_000], new_out(1)) == esi.ESI_ERR_OUT_OF_BOUNDS
+        S1, T1 = e.get_state()
+        assert S1.tobytes() == S0.tobytes() and T1.tobytes() == T0.tobytes()
+        assert e.error() == esi.ESI_ERR_OUT_OF_BOUNDS                    # sticky until reset
+    finally:
+        e.close()
 
 
 def test_checkpoint_resume_equals_whole_stream_bit_exact_on_sparse_pixels():
@@ -378,6 +447,51 @@ def test_c4_full_size_sampled():
     assert_state_close(S.reshape(-1)[pix], T.reshape(-1)[pix], S_ref[0], T_ref[0])
     # every pixel: frame values in range, state within the clamp bounds
     assert float(np.abs(S).max()) <= w.params["s_max"] + 1e-6
+
+
+def _prefix_check(w, t_end, fps):
+    """Full-frame parity of the first t_end us of workload w (events with
+    t <= t_end, frames of the fps grid up to t_end) against the oracle, in the
+    launch configuration bench.py times (default handle, device events/out)."""
+    from esi_synth import frame_times
+    ev_np = to_numpy_struct(w.events)
+    n = int(np.searchsorted(ev_np["t"], t_end, side="right"))
+    ev_np = ev_np[:n]
+    tf = frame_times(t_end, fps)
+    f_gpu, S_gpu, T_gpu, _ = gpu_run(w.W, w.H, from_numpy_struct(ev_np), tf, w.params)
+    f_ref, S_ref, T_ref = oracle_run(w.W, w.H, ev_np, tf, w.params)
+    assert_state_close(S_gpu, T_gpu, S_ref, T_ref)
+    return assert_frames_close(f_gpu, f_ref), n
+
+
+def test_c4_first_1_5_s_full_frames():
+    """c4 (1280x720), first 1.5 s including the 100 Mev/s burst at 0.5-0.55 s:
+    every pixel of every frame (150 @100 FPS) and the final state against the
+    oracle (VERDICT r1 'next' item 2)."""
+    w = make_workload("c4", "cuda")
+    frac, n = _prefix_check(w, 1_500_000, 100)
+    assert n > 20_000_000
+
+
+def test_c4_1000_fps_full_frames():
+    """c4 at 1000 FPS readout over the first 0.6 s (the burst included): 600
+    full frames against the oracle."""
+    w = make_workload("c4", "cuda")
+    _prefix_check(w, 600_000, 1000)
+
+
+def test_2560x1440_sensor_full_frames():
+    """A 2560x1440 sensor (c5b scene at 80 Mev/s, first 0.5 s) on one GPU:
+    band_px = 4096 and 900 bands, every pixel of 50 frames against the oracle."""
+    from paper_2508_02238_b200 import Esi
+    w = make_workload("c5b", "cuda", duration_us=500_000)
+    e = Esi(w.W, w.H, **w.params)
+    try:
+        nb, bp, nw = e.layout()
+        assert bp == 4096 and nb == 900 and nw == 16
+    finally:
+        e.close()
+    _prefix_check(w, 500_000, 100)
 
 
 def test_c2_at_1000_fps():
