@@ -260,11 +260,16 @@ def make_stream(name, rank, idx, args):
     return make_workload("c5a", "cuda", seed=seed)
 
 
-def run_streams(args, ctx, peaks):
-    from paper_2508_02238_b200 import Esi
+def run_streams(args, ctx, peaks, handle_factory=None, stream_factory=None):
+    """c4 / c5a: stream sharding.  handle_factory / stream_factory are injectable
+    (the gloo CPU test of the multi-rank orchestration uses stand-ins)."""
+    if handle_factory is None:
+        from paper_2508_02238_b200 import Esi as handle_factory
+    stream_factory = stream_factory or make_stream
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback 6.65 TB/s"
     rank, world = ctx.rank, ctx.world
+    cuda = ctx.device == "cuda"
     if args.config == "c4":
         n_streams, n_distinct = 1, 1
     else:
@@ -273,16 +278,17 @@ def run_streams(args, ctx, peaks):
         n_streams = 64 // world
         n_distinct = min(n_streams, args.c5a_distinct)
     t0 = time.time()
-    ws = [make_stream(args.config, rank, i, args) for i in range(n_distinct)]
-    torch.cuda.synchronize()
+    ws = [stream_factory(args.config, rank, i, args) for i in range(n_distinct)]
+    ctx.sync()
     gen_s = time.time() - t0
     w = ws[0]
     F = len(w.t_frames)
-    stream = torch.cuda.Stream()
+    stream = torch.cuda.Stream() if cuda else None
     validate = 1 if args.validation == "push" else 0
-    e = Esi(w.W, w.H, validate_on_push=validate, **w.params)
-    e.set_stream(stream.cuda_stream)
-    outs = [torch.empty((F, w.H, w.W), dtype=torch.uint8, device="cuda") for _ in range(min(2, n_streams))]
+    e = handle_factory(w.W, w.H, validate_on_push=validate, **w.params)
+    if cuda:
+        e.set_stream(stream.cuda_stream)
+    outs = [torch.empty((F, w.H, w.W), dtype=torch.uint8, device=ctx.device) for _ in range(min(2, n_streams))]
     events_step = sum(ws[s % n_distinct].n for s in range(n_streams))
     frames_step = F * n_streams
 
@@ -296,9 +302,10 @@ def run_streams(args, ctx, peaks):
 
     for _ in range(args.warmup):
         step()
-    with ClockSampler(ctx.local) as clk:
+    with ClockSampler(ctx.local, enabled=cuda) as clk:
         step()                      # keeps the GPU busy while nvidia-smi starts
-        time.sleep(0.5)
+        if cuda:
+            time.sleep(0.5)
         step()
         t_wall0 = time.time()
         ms_total = ctx.timed(step, args.steps, stream)
@@ -310,9 +317,9 @@ def run_streams(args, ctx, peaks):
         e.enable_kernel_timing(kt_steps > 0)
         kt_ms = ctx.timed(step, kt_steps, stream) if kt_steps else None
     ms_step = ms_total / args.steps
-    events_total = sum_over_ranks(events_step, world) * args.steps
+    events_total = sum_over_ranks(events_step, world, ctx.device) * args.steps
     value = events_total / (ms_total / 1e3)
-    frames_per_s = sum_over_ranks(frames_step, world) * args.steps / (ms_total / 1e3)
+    frames_per_s = sum_over_ranks(frames_step, world, ctx.device) * args.steps / (ms_total / 1e3)
     n_chunks = max(1, stats["chunks"])
     roof, k_ms = roofline_of(e, w, F, n_chunks, kt_steps * n_streams, hbm_peak, peak_src)
     e.enable_kernel_timing(False)
@@ -328,18 +335,20 @@ def run_streams(args, ctx, peaks):
     # the other validation mode, a short pass (same workload)
     if args.config == "c4" and not args.no_alt_validation:
         e.close()
-        e = Esi(w.W, w.H, validate_on_push=1 - validate, **w.params)
-        e.set_stream(stream.cuda_stream)
+        e = handle_factory(w.W, w.H, validate_on_push=1 - validate, **w.params)
+        if cuda:
+            e.set_stream(stream.cuda_stream)
         step()
-        ms_alt = ctx.timed(step, max(1, min(args.steps, 5)), stream) / max(1, min(args.steps, 5))
+        n_alt = max(1, min(args.steps, 5))
+        ms_alt = ctx.timed(step, n_alt, stream) / n_alt
         extra["other_validation_mode"] = {
             "validation": "fused" if validate else "push",
-            "value": sum_over_ranks(events_step, world) / (ms_alt / 1e3), "ms_per_step": ms_alt,
+            "value": sum_over_ranks(events_step, world, ctx.device) / (ms_alt / 1e3), "ms_per_step": ms_alt,
             "note": ("validate_on_push=0: the checks run inside the ingest kernel K1 (no extra read of the "
                      "events); a failing render restores S/T, its frames are unspecified (DESIGN reading A21)")
             if validate else "validate_on_push=1: atomic push, one extra read of the events"}
     e2e = None
-    if args.e2e_steps > 0 and args.config == "c4":
+    if args.e2e_steps > 0 and args.config == "c4" and cuda:
         e2e = run_e2e(args, ctx, w, stream)
     e.close()
     cfg = stream_config(w, world, args, n_streams, n_distinct)
@@ -575,6 +584,15 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def bench_line(args, res, world, cpu=None, lat=None):
+    res = dict(res)
+    return {"metric": METRIC, "value": res.pop("value"), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res.pop("ms_per_step"),
+            "higher_is_better": True, "scaling": res.pop("scaling"), "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": res.pop("config"), "frames_per_s": res.pop("frames_per_s"),
+            "cpu_baseline": cpu, "latency": lat, **res}
+
+
 def parse_args(argv):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -620,12 +638,7 @@ def main(argv=None):
         if rank == 0 and world == 1 and not args.no_latency and args.config == "c4":
             lat = run_latency(args)
         if rank == 0:
-            line = {"metric": METRIC, "value": res.pop("value"), "unit": UNIT, "n_gpus": world,
-                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": res.pop("ms_per_step"),
-                    "higher_is_better": True, "scaling": res.pop("scaling"), "vs_baseline": None, "dtype": "f32",
-                    "data": "synthetic", "config": res.pop("config"), "frames_per_s": res.pop("frames_per_s"),
-                    "cpu_baseline": cpu, "latency": lat, **res}
-            print(json.dumps(line), flush=True)
+            print(json.dumps(bench_line(args, res, world, cpu, lat)), flush=True)
     import torch.distributed as dist
     if dist.is_initialized():
         dist.destroy_process_group()

@@ -103,22 +103,30 @@ cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int
   return cudaGetLastError();
 }
 
-__global__ void esi_validate_kernel(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
-                                    int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
-                                    unsigned long long* err) {
+__global__ void __launch_bounds__(256) esi_validate_kernel(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
+                                                           int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
+                                                           unsigned long long* err) {
+  // One 16-byte load per event; the predecessor's t comes from the neighbouring
+  // lane (lane 0 loads it), so each event record is read once.
   const int4* evv = reinterpret_cast<const int4*>(ev);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int4 r = ld_stream16(evv + i);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool in = i < n;
+    const int4 r = in ? ld_stream16(evv + i) : make_int4(0, 0, 0, 0);
     const int64_t t = (int64_t)(((uint64_t)(uint32_t)r.y << 32) | (uint32_t)r.x);
+    int64_t tp = __shfl_up_sync(0xffffffffu, t, 1);
+    if (lane == 0 && in) tp = i > 0 ? ev[i - 1].t_us : *prev_t;
     const uint32_t x = (uint32_t)r.z & 0xffffu, y = (uint32_t)r.z >> 16;
     const int p = (int)(int8_t)(r.w & 0xff);
-    const int64_t tp = i > 0 ? ev[i - 1].t_us : *prev_t;
-    int code = 0;
-    if (x >= (uint32_t)W || y >= (uint32_t)H) code = ESI_ERR_OUT_OF_BOUNDS;
-    else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
-    else if (t < t_origin || t < tp || t <= last_frame_t) code = ESI_ERR_NEGATIVE_INTERVAL;
-    if (code) atomicMin(err, ((unsigned long long)i << 8) | (unsigned)code);
+    if (in && ((x >= (uint32_t)W) | (y >= (uint32_t)H) | (p * p != 1) | (t < t_origin) | (t < tp) | (t <= last_frame_t))) {
+      int code;
+      if (x >= (uint32_t)W || y >= (uint32_t)H) code = ESI_ERR_OUT_OF_BOUNDS;
+      else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
+      else code = ESI_ERR_NEGATIVE_INTERVAL;
+      atomicMin(err, ((unsigned long long)i << 8) | (unsigned)code);
+    }
   }
 }
 
@@ -127,7 +135,7 @@ cudaError_t launch_validate(const esi_event_t* ev, int64_t n, const int64_t* pre
                             unsigned long long* err, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
   esi_validate_kernel<<<(int)blocks, 256, 0, s>>>(ev, n, prev_t, t_origin, last_frame_t, W, H, err);
   return cudaGetLastError();
 }

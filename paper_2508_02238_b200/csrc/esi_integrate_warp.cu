@@ -38,41 +38,37 @@ namespace {
 #include "esi_fast_common.cuh"
 
 constexpr int kW2MaxWarps = 16;
+constexpr int kW2SB = 3072;                   // events per sub-batch (compile time: constant smem offsets)
 
+// Shared memory of one CTA.  The sub-batch arrays sit at constant offsets (no
+// address registers); the band arrays follow at run-time offsets.
 struct W2Smem {
   float* S;        // [bp] accumulation
   float* T;        // [bp] last time relative to trel
   uint32_t* M;     // [bp] per-pixel peer masks of one warp round (zero between rounds)
-  uint2* buf[2];   // [sb] gathered sub-batches, arrival order
-  uint2* list;     // [sb] the sub-batch split by owner warp (owner-major, arrival-minor)
-  uint16_t* key;   // [sb] owner << 11 | rank of each gathered event
-  uint32_t* om;    // [kW2MaxWarps][16] owner peer masks of the count pass
-  uint32_t* cnt;   // [kW2MaxWarps][16] events per (slice warp, owner)
   uint32_t* pre;   // [n_tiles + 1] band events before tile t
   uint16_t* mo;    // [n_tiles] offset of the band's run inside tile t
 };
+constexpr size_t kW2Cur = 0;                                  // uint2 [kW2SB] gathered sub-batch, arrival order
+constexpr size_t kW2List = kW2Cur + (size_t)kW2SB * 8;        // uint2 [kW2SB] split by owner (owner-major)
+constexpr size_t kW2Key = kW2List + (size_t)kW2SB * 8;        // u16 [kW2SB] owner << 12 | rank
+constexpr size_t kW2Cnt = kW2Key + (size_t)kW2SB * 2;         // u32 [kW2MaxWarps][16] events per (slice, owner)
+constexpr size_t kW2Band = kW2Cnt + (size_t)kW2MaxWarps * 16 * 4;
 
-__host__ __device__ inline size_t w2_smem_bytes(int bp, int sb, int n_tiles) {
+__host__ __device__ inline size_t w2_smem_bytes(int bp, int n_tiles) {
   const size_t b = (size_t)((bp + 3) & ~3);
-  return b * 12 + (size_t)sb * (8 * 3 + 2) + 2 * kW2MaxWarps * 16 * 4 + (size_t)(n_tiles + 1) * 4 +
-         (((size_t)n_tiles * 2 + 15) & ~(size_t)15) + 64;
+  return kW2Band + b * 12 + (size_t)(n_tiles + 1) * 4 + (((size_t)n_tiles * 2 + 15) & ~(size_t)15) + 16;
 }
 
-__device__ __forceinline__ W2Smem w2_carve(unsigned char* base, int bp, int sb, int n_tiles) {
+__device__ __forceinline__ W2Smem w2_carve(unsigned char* base, int bp, int n_tiles) {
   W2Smem m;
-  unsigned char* q = base;
+  unsigned char* q = base + kW2Band;
   const int b4 = (bp + 3) & ~3;
-  m.buf[0] = reinterpret_cast<uint2*>(q); q += (size_t)sb * 8;
-  m.buf[1] = reinterpret_cast<uint2*>(q); q += (size_t)sb * 8;
-  m.list = reinterpret_cast<uint2*>(q); q += (size_t)sb * 8;
   m.S = reinterpret_cast<float*>(q); q += (size_t)b4 * 4;
   m.T = reinterpret_cast<float*>(q); q += (size_t)b4 * 4;
   m.M = reinterpret_cast<uint32_t*>(q); q += (size_t)b4 * 4;
-  m.om = reinterpret_cast<uint32_t*>(q); q += kW2MaxWarps * 16 * 4;
-  m.cnt = reinterpret_cast<uint32_t*>(q); q += kW2MaxWarps * 16 * 4;
   m.pre = reinterpret_cast<uint32_t*>(q); q += (size_t)(n_tiles + 1) * 4;
-  m.mo = reinterpret_cast<uint16_t*>(q); q += ((size_t)n_tiles * 2 + 15) & ~(size_t)15;
-  m.key = reinterpret_cast<uint16_t*>(q);
+  m.mo = reinterpret_cast<uint16_t*>(q);
   return m;
 }
 
@@ -188,20 +184,24 @@ template <int BM>
 __global__ void __launch_bounds__(kW2MaxWarps * 32) esi_integrate_w2_kernel(IntArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_wsum[32];
+  uint2* const cur = reinterpret_cast<uint2*>(smem_raw + kW2Cur);
+  uint2* const lst = reinterpret_cast<uint2*>(smem_raw + kW2List);
+  uint16_t* const key = reinterpret_cast<uint16_t*>(smem_raw + kW2Key);
+  uint32_t* const cnt = reinterpret_cast<uint32_t*>(smem_raw + kW2Cnt);
   const int nw = (int)(blockDim.x >> 5), nthr = (int)blockDim.x;
   const int band = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bp = a.band_px, sb = a.w2_sb;
+  const int bp = a.band_px;
   const int64_t px0 = (int64_t)band * bp;
   const int npx = (int)min((int64_t)bp, a.P - px0);
   const int n_tiles = a.n_tiles;
-  const W2Smem sm = w2_carve(smem_raw, bp, sb, n_tiles);
 
   if (a.gate && *a.gate != kNoError) return;   // lazy validation found an invalid event: write nothing
   const ChunkInfo ci = *a.info;
   const int f_lo = ci.f_lo, f_hi = ci.f_hi;
   const bool active = ci.active != 0;
   if (!active && f_lo >= f_hi) return;
+  const W2Smem sm = w2_carve(smem_raw, bp, n_tiles);
   const int64_t trel = ci.trel;
   const uint32_t trel32 = (uint32_t)trel;
   const float t_clamp = -(float)(a.dp.dt_cut + 1);
@@ -214,7 +214,6 @@ __global__ void __launch_bounds__(kW2MaxWarps * 32) esi_integrate_w2_kernel(IntA
     sm.T[i] = in ? (float)max(a.T[px0 + i] - trel, (int64_t)t_clamp) : t_clamp;
     sm.M[i] = 0u;
   }
-  for (int i = threadIdx.x; i < kW2MaxWarps * 16; i += nthr) sm.om[i] = 0u;
   int n_b = 0;
   if (active) {
     const uint32_t* meta = a.meta + (int64_t)band * n_tiles;
@@ -253,47 +252,47 @@ __global__ void __launch_bounds__(kW2MaxWarps * 32) esi_integrate_w2_kernel(IntA
   const int nq_band = (npx + 3) >> 2;
   const int q0 = min(warp * a.w2_qpw, nq_band), q1 = min(q0 + a.w2_qpw, nq_band);
   const uint32_t qmagic = a.w2_qmagic;   // (q * qmagic) >> 32 == q / qpw for q < 2^12
+  // lane o < 16 counts owner o: its bits as all-ones / all-zero masks
+  const unsigned lb0 = (lane & 1) ? kFull : 0u, lb1 = (lane & 2) ? kFull : 0u;
+  const unsigned lb2 = (lane & 4) ? kFull : 0u, lb3 = (lane & 8) ? kFull : 0u;
+  // slice of the sub-batch this warp splits: [warp * per, (warp + 1) * per)
+  const int per_full = (((kW2SB + nw - 1) / nw) + 31) & ~31;
 
   int j = f_lo;
   bool done = false;
-  if (n_b > 0) w2_gather(a.rec, sm.pre, sm.mo, n_tiles, n_b, 0, sb, sm.buf[0], warp, nw, lane);
-  for (int sb0 = 0, kb = 0; sb0 < n_b && !done; sb0 += sb, ++kb) {
-    const int n_sb = min(sb, n_b - sb0);
-    const uint2* cur = (kb & 1) ? sm.buf[1] : sm.buf[0];
+  if (n_b > 0) w2_gather(a.rec, sm.pre, sm.mo, n_tiles, n_b, 0, kW2SB, cur, warp, nw, lane);
+  for (int sb0 = 0; sb0 < n_b && !done; sb0 += kW2SB) {
+    const int n_sb = min(kW2SB, n_b - sb0);
     cp_async_wait_all();
-    __syncthreads();                                   // [A] cur complete; lists free
-    if (sb0 + sb < n_b)
-      w2_gather(a.rec, sm.pre, sm.mo, n_tiles, n_b, sb0 + sb, sb, (kb & 1) ? sm.buf[0] : sm.buf[1], warp, nw,
-                lane);
-    // ---- split, count pass: warp `warp` ranks the slice [i0, i1) by owner
-    const int per = (((n_sb + nw - 1) / nw) + 31) & ~31;
+    __syncthreads();                                   // [A] cur complete; every warp is done with lst
+    // ---- split, count pass: warp `warp` ranks the slice [i0, i1) by owner (4 ballots:
+    // the peers of a lane are the lanes whose owner bits all match; ranks = lane order)
+    const int per = n_sb == kW2SB ? per_full : (((n_sb + nw - 1) / nw) + 31) & ~31;
     const int i0 = min(warp * per, n_sb), i1 = min(i0 + per, n_sb);
-    uint32_t* om = sm.om + warp * 16;
     uint32_t cnt_o = 0;                                // lane o < 16: events of owner o so far
     for (int i = i0; i < i1; i += 32) {
       const int idx = i + lane;
       const bool valid = idx < i1;
       const uint32_t px = valid ? (cur[idx].y & 0x7fffffffu) : 0u;
       const uint32_t owner = (uint32_t)(((uint64_t)(px >> 2) * qmagic) >> 32);
-      if (valid) atomicOr(&om[owner], 1u << lane);
-      __syncwarp();
-      const uint32_t mine = lane < 16 ? om[lane] : 0u;
-      const uint32_t peers = valid ? om[owner] : 0u;
-      __syncwarp();
-      if (lane < 16) om[lane] = 0u;
-      const uint32_t before = cnt_o;
+      const unsigned vm = __ballot_sync(kFull, valid);
+      const unsigned b0 = __ballot_sync(kFull, owner & 1u), b1 = __ballot_sync(kFull, owner & 2u);
+      const unsigned b2 = __ballot_sync(kFull, owner & 4u), b3 = __ballot_sync(kFull, owner & 8u);
+      const unsigned ob0 = (owner & 1u) ? kFull : 0u, ob1 = (owner & 2u) ? kFull : 0u;
+      const unsigned ob2 = (owner & 4u) ? kFull : 0u, ob3 = (owner & 8u) ? kFull : 0u;
+      const unsigned peers = vm & ~(b0 ^ ob0) & ~(b1 ^ ob1) & ~(b2 ^ ob2) & ~(b3 ^ ob3);
+      const unsigned mine = vm & ~(b0 ^ lb0) & ~(b1 ^ lb1) & ~(b2 ^ lb2) & ~(b3 ^ lb3);
+      const uint32_t base = __shfl_sync(kFull, cnt_o, (int)owner);
       cnt_o += __popc(mine);
-      const uint32_t base = __shfl_sync(kFull, before, (int)(owner & 15u));
-      if (valid) sm.key[idx] = (uint16_t)((owner << 11) | (base + __popc(peers & lanemask_lt())));
-      __syncwarp();
+      if (valid) key[idx] = (uint16_t)((owner << 12) | (base + __popc(peers & lanemask_lt())));
     }
-    if (lane < 16) sm.cnt[warp * 16 + lane] = cnt_o;
+    if (lane < 16) cnt[warp * 16 + lane] = cnt_o;
     __syncthreads();                                   // [B] counts complete
     // list of owner o starts at start_o = sum_{o' < o} col_o'; this slice's run of it at + part
     uint32_t col = 0, part = 0;
     if (lane < nw)
       for (int w = 0; w < nw; ++w) {
-        const uint32_t c = sm.cnt[w * 16 + lane];
+        const uint32_t c = cnt[w * 16 + lane];
         col += c;
         part += (w < warp) ? c : 0u;
       }
@@ -308,19 +307,20 @@ __global__ void __launch_bounds__(kW2MaxWarps * 32) esi_integrate_w2_kernel(IntA
     for (int i = i0; i < i1; i += 32) {
       const int idx = i + lane;
       const bool valid = idx < i1;
-      const uint32_t k = valid ? sm.key[idx] : 0u;
-      const uint32_t pos = __shfl_sync(kFull, wpos, (int)(k >> 11)) + (k & 2047u);
+      const uint32_t k = valid ? key[idx] : 0u;
+      const uint32_t pos = __shfl_sync(kFull, wpos, (int)(k >> 12)) + (k & 4095u);
       if (valid) {
         ESI_DCHECK(pos < (uint32_t)n_sb);
-        sm.list[pos] = cur[idx];
+        lst[pos] = cur[idx];
       }
     }
     const int ls = (int)__shfl_sync(kFull, start, warp);
     const int le = ls + (int)__shfl_sync(kFull, col, warp);
-    __syncthreads();                                   // [C] lists complete
-    // ---- process this warp's own list: windows that close inside the sub-batch
-    const bool last_sb = sb0 + sb >= n_b;
+    const bool last_sb = sb0 + kW2SB >= n_b;
     const int32_t t_last = (int32_t)(cur[n_sb - 1].x - trel32);
+    __syncthreads();                                   // [C] lists complete; cur is free
+    if (!last_sb) w2_gather(a.rec, sm.pre, sm.mo, n_tiles, n_b, sb0 + kW2SB, kW2SB, cur, warp, nw, lane);
+    // ---- process this warp's own list: windows that close inside the sub-batch
     int e = ls;
     while (true) {
       bool closed = false;
@@ -334,11 +334,11 @@ __global__ void __launch_bounds__(kW2MaxWarps * 32) esi_integrate_w2_kernel(IntA
       while (e < le) {                                  // own events with t <= lim, 32 at a time
         const int idx = e + lane;
         bool valid = idx < le;
-        const uint2 r = valid ? sm.list[idx] : make_uint2(0u, 0u);
+        const uint2 r = valid ? lst[idx] : make_uint2(0u, 0u);
         valid = valid && (int32_t)(r.x - trel32) <= lim;
         const int n = __popc(__ballot_sync(kFull, valid));   // the list is time-sorted: a prefix
         if (n == 0) break;
-        w2_apply_round<BM>(sm, sm.list, e, valid, r, trel32, lane, kc);
+        w2_apply_round<BM>(sm, lst, e, valid, r, trel32, lane, kc);
         e += n;
         if (n < 32) break;
       }
@@ -366,13 +366,13 @@ __global__ void __launch_bounds__(kW2MaxWarps * 32) esi_integrate_w2_kernel(IntA
 
 template <int BM>
 cudaError_t launch_w2_b(const IntArgs& a, cudaStream_t s) {
-  const size_t smem = w2_smem_bytes(a.band_px, a.w2_sb, a.n_tiles);
+  const size_t smem = w2_smem_bytes(a.band_px, a.n_tiles);
   int dev = 0;
   cudaGetDevice(&dev);
   static int configured[64] = {0};   // per device: the attribute is per context
   if (dev < 0 || dev >= 64 || !configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(esi_integrate_w2_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)w2_smem_bytes(kMaxBandPx, 2048, kMaxTilesPerChunk));
+                                         (int)w2_smem_bytes(kMaxBandPx, kMaxTilesPerChunk));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev] = 1;
   }
@@ -382,7 +382,7 @@ cudaError_t launch_w2_b(const IntArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-size_t integrate_w2_smem_bytes(int band_px, int sb, int n_tiles) { return w2_smem_bytes(band_px, sb, n_tiles); }
+size_t integrate_w2_smem_bytes(int band_px, int n_tiles) { return w2_smem_bytes(band_px, n_tiles); }
 
 cudaError_t launch_integrate_w2(const IntArgs& a, cudaStream_t s) {
   if (a.dp.first)

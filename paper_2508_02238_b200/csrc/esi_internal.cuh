@@ -102,6 +102,9 @@ struct PartArgs {
   int32_t W, H;
   int32_t band_px, nb;
   uint64_t band_magic;       // pid / band_px = (pid * band_magic) >> 40 (exact for pid < 2^23)
+  uint32_t band_magic32;     // pid / band_px = umulhi(pid, band_magic32) when band32 (checked on the host)
+  int32_t band32;
+  int32_t validate;          // 1: check every event (fused validation); 0: validated on push
   uint2* rec;                // [n_tiles * kTile] tile-local band-sorted records
   uint32_t* meta;            // [nb][n_tiles]: offset | count << 16
   int64_t* tile_t0;          // [n_tiles]
@@ -166,10 +169,10 @@ struct RouteRows {
   int32_t start[65];
 };
 
-size_t partition_smem_bytes(int nb);
+size_t partition_smem_bytes(int nb, int rank_mode);
 size_t integrate_smem_bytes(int band_px);
 size_t integrate_fast_smem_bytes(int band_px, int n_tiles);
-cudaError_t launch_partition(const PartArgs& a, int n_tiles, bool atomic_rank, cudaStream_t s);
+cudaError_t launch_partition(const PartArgs& a, int n_tiles, int rank_mode, cudaStream_t s);
 cudaError_t probe_atomic_order(unsigned* d_bad, cudaStream_t s);
 cudaError_t launch_integrate(const IntArgs& a, cudaStream_t s);
 cudaError_t launch_readout(const ReadoutArgs& a, cudaStream_t s);
@@ -181,7 +184,7 @@ cudaError_t launch_plan(const esi_event_t* const* chunk_first, const int64_t* ch
 cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s);
 // warp-owned fast kernel (32-bit relative times, dt_cut < 2^23) -- esi_integrate_warp.cu
 cudaError_t launch_integrate_w2(const IntArgs& a, cudaStream_t s);
-size_t integrate_w2_smem_bytes(int band_px, int sb, int n_tiles);
+size_t integrate_w2_smem_bytes(int band_px, int n_tiles);
 // consume: for segment k, count events with t <= t_cap (binary search), and set
 // *last_t to the t of the last consumed event of the last segment with one.
 cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,

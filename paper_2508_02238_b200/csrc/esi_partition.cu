@@ -18,10 +18,11 @@
 
 namespace esi {
 
-size_t partition_smem_bytes(int nb) {
+size_t partition_smem_bytes(int nb, int rank_mode) {
   const int nbp = (nb + 7) & ~7;
   return (size_t)kTile * sizeof(int4) + (size_t)kPartWarps * nbp * sizeof(uint16_t) +
-         (size_t)(nb + 1) * sizeof(uint32_t) + 64 * sizeof(uint32_t);
+         (size_t)(nb + 1) * sizeof(uint32_t) + 64 * sizeof(uint32_t) +
+         (rank_mode == 2 ? (size_t)kPartWarps * nbp * sizeof(uint32_t) : 0);
 }
 
 // Exclusive scan of v[0..n) in place (n <= 4 * kPartThreads); v[n] = total.
@@ -70,7 +71,7 @@ __device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
 // The tile's raw 16-B records are staged in shared memory with cp.async (every
 // load of the tile in flight at once); the sorted tile later reuses the first
 // half of that buffer, after the records have been consumed into registers.
-template <bool RANK_ATOMIC, bool FULL>
+template <int RANK, bool VALIDATE, bool BAND32, bool FULL>
 __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char* smem, int tile, int ne) {
   constexpr int EPT = kTile / kPartThreads;                      // events per thread (8)
   constexpr int WEV = EPT * 32;                                  // events per warp (256)
@@ -80,6 +81,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   uint16_t* hist = reinterpret_cast<uint16_t*>(raw + kTile);     // [kPartWarps][nbp]
   uint32_t* boff = reinterpret_cast<uint32_t*>(hist + kPartWarps * nbp);  // [nb + 1]
   uint32_t* wsum = boff + a.nb + 1;                               // [64]
+  uint32_t* pmask = wsum + 64;                                    // RANK 2: [kPartWarps][nbp] peer masks (zero)
   __shared__ int s_wide;
   __shared__ int64_t s_tprev;
 
@@ -104,6 +106,8 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   asm volatile("cp.async.commit_group;" ::: "memory");
   for (int i = threadIdx.x; i < kPartWarps * nbp / 8; i += kPartThreads)
     reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (RANK == 2)
+    for (int i = threadIdx.x; i < kPartWarps * nbp; i += kPartThreads) pmask[i] = 0u;
   if (threadIdx.x == 0) s_tprev = tile > 0 ? ev[-1].t_us : *a.prev_t;   // predecessor of the tile's first event
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
@@ -123,26 +127,47 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     uint32_t x = (uint32_t)rw.z & 0xffffu;
     uint32_t y = (uint32_t)rw.z >> 16;
     const int p = (int)(int8_t)(rw.w & 0xff);
-    const int64_t tp = i > 0 ? *reinterpret_cast<const int64_t*>(raw + i - 1) : tprev0;
-    // validation (reading A15), one combined test on the common path
-    const bool bad = (x >= W) | (y >= H) | (p * p != 1) | (t < t_min) | (t < tp);
-    if (act && bad) {
-      int code;
-      if (x >= W || y >= H) code = ESI_ERR_OUT_OF_BOUNDS;
-      else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
-      else code = ESI_ERR_NEGATIVE_INTERVAL;
-      atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + i) << 8) | (unsigned)code);
-      x = 0; y = 0;              // keep the pipeline well-defined; the call reports the error
+    bool bad = false;
+    if (VALIDATE) {
+      const int64_t tp = i > 0 ? *reinterpret_cast<const int64_t*>(raw + i - 1) : tprev0;
+      // validation (reading A15), one combined test on the common path
+      bad = (x >= W) | (y >= H) | (p * p != 1) | (t < t_min) | (t < tp);
+      if (act && bad) {
+        int code;
+        if (x >= W || y >= H) code = ESI_ERR_OUT_OF_BOUNDS;
+        else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
+        else code = ESI_ERR_NEGATIVE_INTERVAL;
+        atomicMin(a.err, ((unsigned long long)(a.index_base + e0 + i) << 8) | (unsigned)code);
+        x = 0; y = 0;              // keep the pipeline well-defined; the call reports the error
+      }
     }
     const uint32_t pid = y * W + x;
-    const uint32_t band = act ? (uint32_t)(((uint64_t)pid * a.band_magic) >> 40) : 0u;
+    // pid / band_px: 32-bit high multiply when exact for every pid of the sensor, else 64-bit
+    const uint32_t band = !act ? 0u : BAND32 ? __umulhi(pid, a.band_magic32)
+                                            : (uint32_t)(((uint64_t)pid * a.band_magic) >> 40);
     const uint32_t pix = pid - band * BPX;
     uint32_t rank;
-    if (RANK_ATOMIC) {
+    if (RANK == 1) {
       uint32_t* hw = reinterpret_cast<uint32_t*>(myhist);
       const uint32_t sh = (band & 1u) << 4;
       const uint32_t old = act ? atomicAdd(hw + (band >> 1), 1u << sh) : 0u;
       rank = (old >> sh) & 0xffffu;
+    } else if (RANK == 2) {
+      // peers = the lanes of this round with my band: OR of lane bits into the warp's
+      // mask of the band (order-independent), so ranks are lane (= arrival) order by construction
+      uint32_t* pm = pmask + warp * nbp;
+      if (act) atomicOr(pm + band, 1u << lane);
+      __syncwarp();
+      const uint32_t peers = act ? pm[band] : 0u;
+      const uint32_t below = peers & lanemask_lt();
+      const uint32_t base = act ? (uint32_t)myhist[band] : 0u;
+      __syncwarp();
+      if (act && below == 0u) {                  // lowest peer: advance the histogram, clear the mask
+        myhist[band] = (uint16_t)(base + __popc(peers));
+        pm[band] = 0u;
+      }
+      __syncwarp();
+      rank = base + __popc(below);
     } else {
       // warp multi-split: lanes whose band equals mine
       unsigned peers = __ballot_sync(kFull, act);
@@ -232,35 +257,43 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // copy complete before the CTA retires
 }
 
-template <bool RANK_ATOMIC>
+template <int RANK, bool VALIDATE, bool BAND32>
 __global__ void __launch_bounds__(kPartThreads, kPartCtas) esi_partition_kernel(PartArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   // Chunk entirely after the last frame of this render: nothing to integrate.
   if (a.ev[0].t_us > a.t_cap) return;
   const int tile = blockIdx.x;
   const int ne = (int)min((int64_t)kTile, a.n - (int64_t)tile * kTile);
-  if (ne == kTile) partition_tile<RANK_ATOMIC, true>(a, smem, tile, ne);
-  else partition_tile<RANK_ATOMIC, false>(a, smem, tile, ne);
+  if (ne == kTile) partition_tile<RANK, VALIDATE, BAND32, true>(a, smem, tile, ne);
+  else partition_tile<RANK, VALIDATE, BAND32, false>(a, smem, tile, ne);
 }
 
-template <bool RA>
+template <int RA, bool V, bool B32>
 static cudaError_t launch_part_t(const PartArgs& a, int n_tiles, cudaStream_t s) {
-  const size_t smem = partition_smem_bytes(a.nb);
+  const size_t smem = partition_smem_bytes(a.nb, RA);
   int dev = 0;
   cudaGetDevice(&dev);
   static int configured[64] = {0};   // per device (the attribute is per context); the maximum once
   if (dev < 0 || dev >= 64 || !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel<RA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)partition_smem_bytes(kMaxBands));
+    cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel<RA, V, B32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)partition_smem_bytes(kMaxBands, RA));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev] = 1;
   }
-  esi_partition_kernel<RA><<<n_tiles, kPartThreads, smem, s>>>(a);
+  esi_partition_kernel<RA, V, B32><<<n_tiles, kPartThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_partition(const PartArgs& a, int n_tiles, bool atomic_rank, cudaStream_t s) {
-  return atomic_rank ? launch_part_t<true>(a, n_tiles, s) : launch_part_t<false>(a, n_tiles, s);
+template <int RA>
+static cudaError_t launch_part_r(const PartArgs& a, int n_tiles, cudaStream_t s) {
+  if (a.validate) return a.band32 ? launch_part_t<RA, true, true>(a, n_tiles, s) : launch_part_t<RA, true, false>(a, n_tiles, s);
+  return a.band32 ? launch_part_t<RA, false, true>(a, n_tiles, s) : launch_part_t<RA, false, false>(a, n_tiles, s);
+}
+
+cudaError_t launch_partition(const PartArgs& a, int n_tiles, int rank_mode, cudaStream_t s) {
+  return rank_mode == 1 ? launch_part_r<1>(a, n_tiles, s)
+         : rank_mode == 2 ? launch_part_r<2>(a, n_tiles, s)
+                          : launch_part_r<0>(a, n_tiles, s);
 }
 
 // Probe: do warp-wide shared-memory atomicAdds on one address return values in

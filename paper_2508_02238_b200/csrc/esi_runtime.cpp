@@ -105,7 +105,11 @@ struct esi_handle {
   std::vector<TimedLaunch> timed;
   std::vector<cudaEvent_t> ev_pool;
   int64_t st_launches = 0, st_events = 0, st_chunks = 0, st_fast = 0;
-  bool atomic_rank = true;   // K1 ranks from lane-ordered smem atomics (probed at create)
+  bool atomic_rank = true;   // lane-ordered smem atomics observed (probed at create)
+  int rank_mode = 2;         // K1 stable ranks: 2 = peer masks (ordered by construction, default),
+                             // 1 = lane-ordered atomics (only if probed), 0 = ballot multi-split
+  uint32_t band_magic32 = 0;
+  bool band32 = false;
   bool allow_fast = true;    // K2 fast variant allowed (dt_cut < 2^23)
   bool single_stream = false; // ESI_SINGLE_STREAM=1: K1 and K2 on one stream
   bool k2_warp = true;        // K2 = warp-owned kernel (esi_integrate_warp.cu); ESI_K2=block: the older
@@ -403,14 +407,15 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
     h->w2_qmagic = (uint32_t)((((uint64_t)1) << 32) / (uint64_t)h->w2_qpw + 1);
     for (uint32_t q = 0; q < 1024; ++q)   // exactness of the owner division (checked once)
       if ((uint32_t)(((uint64_t)q * h->w2_qmagic) >> 32) != q / (uint32_t)h->w2_qpw) { delete h; return ESI_ERR_INVALID_ARG; }
-    h->w2_sb = 2048;
-    if (const char* e = getenv("ESI_K2_SB")) {
-      const int v = atoi(e);
-      if (v >= 256 && v <= 2048 && v % 32 == 0) h->w2_sb = v;
-    }
   }
   h->nb = (int)((P + h->band_px - 1) / h->band_px);
   h->band_magic = ((uint64_t)1 << 40) / (uint64_t)h->band_px + 1;   // exact pid / band_px for pid < 2^23
+  {  // 32-bit variant: umulhi(pid, m) == pid / bp for all pid < P when (m bp - 2^32) (P - 1) < 2^32
+    const uint64_t m = ((((uint64_t)1) << 32) + (uint64_t)h->band_px - 1) / (uint64_t)h->band_px;
+    const uint64_t err = m * (uint64_t)h->band_px - (((uint64_t)1) << 32);
+    h->band32 = m <= 0xffffffffull && err * (uint64_t)(P - 1) < (((uint64_t)1) << 32);
+    h->band_magic32 = h->band32 ? (uint32_t)m : 0u;
+  }
   int64_t ce = prm.chunk_events > 0 ? prm.chunk_events : (int64_t)8 << 20;
   ce = ((ce + kTile - 1) / kTile) * kTile;
   ce = std::min<int64_t>(ce, (int64_t)kMaxTilesPerChunk * kTile);
@@ -466,7 +471,9 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
       h->atomic_rank = false;
     }
     if (d_bad) cudaFree(d_bad);
-    if (mode && strcmp(mode, "ballot") == 0) h->atomic_rank = false;
+    h->rank_mode = 2;
+    if (mode && strcmp(mode, "ballot") == 0) h->rank_mode = 0;
+    if (mode && strcmp(mode, "atomic") == 0 && h->atomic_rank) h->rank_mode = 1;
   }
   if (!rc && cudaStreamSynchronize(h->stream) != cudaSuccess) rc = ESI_ERR_CUDA;
   if (rc) {
@@ -747,6 +754,9 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.band_px = h->band_px;
       pa.nb = h->nb;
       pa.band_magic = h->band_magic;
+      pa.band_magic32 = h->band_magic32;
+      pa.band32 = h->band32 ? 1 : 0;
+      pa.validate = h->prm.validate_on_push ? 0 : 1;
       pa.rec = h->rec[bf];
       pa.meta = h->meta[bf];
       pa.tile_t0 = h->tile_t0[bf];
@@ -755,7 +765,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.err = h->d_err;
       TimedLaunch t1;
       timed_begin(h, 0, &t1, k1s);
-      ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, k1s));
+      ESI_CUDA(h, launch_partition(pa, n_tiles, h->rank_mode, k1s));
       timed_end(h, &t1);
       if (two || any_host) ESI_CUDA(h, cudaEventRecord(h->ev_k1[bf], k1s));
       if (two) ESI_CUDA(h, cudaStreamWaitEvent(st, h->ev_k1[bf], 0));
@@ -1154,6 +1164,9 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   pa.band_px = h->band_px;
   pa.nb = h->nb;
   pa.band_magic = h->band_magic;
+  pa.band_magic32 = h->band_magic32;
+  pa.band32 = h->band32 ? 1 : 0;
+  pa.validate = h->prm.validate_on_push ? 0 : 1;
   pa.rec = h->rec[0];
   pa.meta = h->meta[0];
   pa.tile_t0 = h->tile_t0[0];
@@ -1161,7 +1174,7 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   pa.wide_t = h->wide_t[0];
   pa.err = h->d_err;
   ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), h->stream));
-  ESI_CUDA(h, launch_partition(pa, n_tiles, h->atomic_rank, h->stream));
+  ESI_CUDA(h, launch_partition(pa, n_tiles, h->rank_mode, h->stream));
   std::vector<uint2> rec(n_tiles * (size_t)kTile);
   std::vector<uint32_t> meta((size_t)h->nb * n_tiles);
   std::vector<int64_t> t0(n_tiles), wt;

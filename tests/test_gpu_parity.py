@@ -80,8 +80,9 @@ def test_c3_hot_pixels():
     check(w.W, w.H, ev_np_of(w), w.t_frames, w.params)
 
 
-def test_c2_ballot_rank_mode(monkeypatch):
-    monkeypatch.setenv("ESI_RANK_MODE", "ballot")
+@pytest.mark.parametrize("mode", ["ballot", "atomic"])
+def test_c2_other_rank_modes(mode, monkeypatch):
+    monkeypatch.setenv("ESI_RANK_MODE", mode)
     w = wl("c2")
     check(w.W, w.H, ev_np_of(w), w.t_frames, w.params, chunk_events=262144)
 
@@ -230,13 +231,18 @@ def test_t_origin_and_late_start():
     check(16, 16, ev, tf, DEF, t_origin=5_000_000_000 - 40_000)
 
 
-@pytest.mark.parametrize("rank_mode", ["auto", "ballot"])
+@pytest.mark.parametrize("rank_mode", ["peers", "ballot", "atomic"])
 def test_partition_is_bit_exact_stable_grouping(rank_mode, monkeypatch):
+    """K1's stable grouping against the plain definition (a stable sort by band,
+    SURVEY P14) in every rank mode: peer masks (default, ordered by
+    construction), ballot multi-split, lane-ordered atomics (probed); uniform
+    streams and streams where 40 % of the events hit one pixel (many lanes of a
+    warp round share a band)."""
     from paper_2508_02238_b200 import Esi
-    if rank_mode == "ballot":
-        monkeypatch.setenv("ESI_RANK_MODE", "ballot")
-    for (W, H, n) in [(64, 48, 100_000), (346, 260, 300_000), (1280, 720, 2_000_000)]:
-        ev = random_stream(W, W, H, n, 1_000_000, cluster=False)
+    monkeypatch.setenv("ESI_RANK_MODE", rank_mode)
+    for (W, H, n, hot) in [(64, 48, 100_000, 0.0), (346, 260, 300_000, 0.0), (1280, 720, 2_000_000, 0.0),
+                           (346, 260, 300_000, 0.4), (1280, 720, 1_000_000, 0.4)]:
+        ev = random_stream(W + int(hot * 10), W, H, n, 1_000_000, hot=hot, cluster=False)
         e = Esi(W, H)
         try:
             e.push(from_numpy_struct(ev).cuda())
@@ -393,7 +399,9 @@ def test_rejected_push_or_render_leaves_state_and_frames_untouched(host_out):
         S0, T0 = e.get_state()
         assert e.push(from_numpy_struct(bad).cuda()) == 0              # accepted lazily
         assert e.render_many_rc([200_000], new_out(1)) == esi.ESI_ERR_OUT_OF_BOUNDS
-        S1, T1 = e.get_state()
+        S1 = np.empty_like(S0)
+        T1 = np.empty_like(T0)
+        assert esi.get_state(e.h, S1, T1) == esi.ESI_ERR_OUT_OF_BOUNDS    # copies, reports the sticky error
         assert S1.tobytes() == S0.tobytes() and T1.tobytes() == T0.tobytes()
         assert e.error() == esi.ESI_ERR_OUT_OF_BOUNDS                    # sticky until reset
     finally:
