@@ -229,7 +229,7 @@ def roofline_of(e, w, F, n_chunks, kt_steps, hbm_peak, peak_src):
     kt_n = {k: kt[k][1] for k in kt}
     P = w.P
     dom = max((0, 1), key=lambda k: kt_ms[k])
-    names = {0: "esi_partition_kernel", 1: "esi_integrate_w2_kernel"}
+    names = {0: "esi_partition_kernel", 1: "esi_integrate_kernel"}
     if dom == 0:
         alg = 16.0 * w.n / n_chunks
         unit_note = "16 B per event read (SURVEY 8(d)) x events per chunk"
@@ -416,8 +416,9 @@ def run_c5b(args, ctx, peaks):
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     b = time_shard_bounds(w.n, world)
+    n_total = w.n
     shard = w.events[b[rank]:b[rank + 1]].contiguous()
-    del w.events
+    w.events = w.events[:0]
     torch.cuda.empty_cache()
     F = len(w.t_frames)
     starts = row_bands(w.H, world)
@@ -455,10 +456,10 @@ def run_c5b(args, ctx, peaks):
         step(stage)
     stage_ms = {k: max_over_ranks(v / n_stage, world) for k, v in stage.items()}
     ms_step = ms_total / args.steps
-    value = w.n * args.steps / (ms_total / 1e3)
+    value = n_total * args.steps / (ms_total / 1e3)
     rows = starts[rank + 1] - starts[rank]
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    band_bytes = 16.0 * (w.n / world) + rows * w.W * F + 24.0 * rows * w.W
+    band_bytes = 16.0 * (n_total / world) + rows * w.W * F + 24.0 * rows * w.W
     asm_bytes = (world - 1) / world * w.P * F
     stages = {
         "route_exchange": {"ms": stage_ms.get("route_exchange"),
@@ -473,8 +474,8 @@ def run_c5b(args, ctx, peaks):
     }
     rb.close()
     cfg = {"workload": f"c5b: {w.W}x{w.H} sensor, first {dur / 1e6:g} s of the 80 Mev/s stream "
-                       f"({w.n} events, {F} frames @100 FPS)",
-           "sensor": f"{w.W}x{w.H}", "events_per_step_per_gpu": w.n / world, "frames_per_step": F,
+                       f"({n_total} events, {F} frames @100 FPS)",
+           "sensor": f"{w.W}x{w.H}", "events_per_step_per_gpu": n_total / world, "frames_per_step": F,
            "esi_params": w.params, "validation": args.validation,
            "parallelism": f"row bands x{world} (router P2P exchange + NCCL frame assembly)"}
     return {"value": value, "ms_per_step": ms_step, "frames_per_s": F * args.steps / (ms_total / 1e3),
@@ -493,7 +494,7 @@ def run_latency(args, frames_max=300):
     from paper_2508_02238_b200 import Esi
     res = {}
     for cfg in ("c2", "c4"):
-        w = make_workload(cfg, "cuda", duration_us=2_000_000) if cfg == "c4" else make_workload(cfg, "cuda")
+        w = make_workload(cfg, "cuda", duration_us=2_000_000) if cfg == "c4" else make_workload(cfg, "cpu")
         ev = w.events.cpu()
         t_all = ev[:, 0].numpy()
         for fps in (100, 1000):

@@ -223,6 +223,19 @@ int esi_ipc_open(int32_t device, const void* handle, void** ptr);
 int esi_ipc_close(int32_t device, void* ptr);
 int esi_stream_sync(int32_t device, void* stream);
 
+/* ---- evaluation: frame vs ground-truth scores --------
+ * SPEC metrics: for each of n_frames 8-bit frames (DEVICE, frame j
+ * at frames + j * n_pixels) the Pearson correlation with the ground-truth
+ * log-intensity field (DEVICE fp32; one field of n_pixels shared by every frame,
+ * or one per frame when truth_per_frame = 1) and the MSE after per-image
+ * zero-mean unit-variance normalisation (= 2 (1 - pearson)).  Scale/offset
+ * invariant, as the paper's relative-intensity claim requires.  A
+ * constant image gives NaN for both ("missing").  pearson / mse_norm:
+ * HOST arrays of n_frames; synchronises `stream`. */
+int esi_frame_metrics(int32_t device, const uint8_t* frames, const float* truth, int64_t n_pixels,
+                      int32_t n_frames, int32_t truth_per_frame, double* pearson, double* mse_norm,
+                      void* stream);
+
 /* ---- instrumentation (used by bench.py and the parity tests) -------------- */
 
 /* Per-kernel device time accumulated by the handle when timing is enabled

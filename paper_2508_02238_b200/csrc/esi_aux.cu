@@ -103,30 +103,47 @@ cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int
   return cudaGetLastError();
 }
 
+__device__ __forceinline__ void validate_one(int64_t i, int64_t n, int4 r, int64_t tp0, int lane, int64_t t_origin,
+                                             int64_t last_frame_t, int32_t W, int32_t H, unsigned long long* err) {
+  const bool in = i < n;
+  const int64_t t = (int64_t)(((uint64_t)(uint32_t)r.y << 32) | (uint32_t)r.x);
+  int64_t tp = __shfl_up_sync(0xffffffffu, t, 1);
+  if (lane == 0) tp = tp0;
+  const uint32_t x = (uint32_t)r.z & 0xffffu, y = (uint32_t)r.z >> 16;
+  const int p = (int)(int8_t)(r.w & 0xff);
+  if (in && ((x >= (uint32_t)W) | (y >= (uint32_t)H) | (p * p != 1) | (t < t_origin) | (t < tp) | (t <= last_frame_t))) {
+    int code;
+    if (x >= (uint32_t)W || y >= (uint32_t)H) code = ESI_ERR_OUT_OF_BOUNDS;
+    else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
+    else code = ESI_ERR_NEGATIVE_INTERVAL;
+    atomicMin(err, ((unsigned long long)i << 8) | (unsigned)code);
+  }
+}
+
+// Eager validation of one push (reading A15).  Four coalesced
+// 16-byte loads in flight per thread (streaming, read once); the predecessor's
+// t comes from the neighbouring lane, lane 0 loads it alongside its own events
+// (issued with them, so a warp waits for one memory latency per 128 events).
 __global__ void __launch_bounds__(256) esi_validate_kernel(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
                                                            int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
                                                            unsigned long long* err) {
-  // One 16-byte load per event; the predecessor's t comes from the neighbouring
-  // lane (lane 0 loads it), so each event record is read once.
+  constexpr int U = 4;
   const int4* evv = reinterpret_cast<const int4*>(ev);
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    const bool in = i < n;
-    const int4 r = in ? ld_stream16(evv + i) : make_int4(0, 0, 0, 0);
-    const int64_t t = (int64_t)(((uint64_t)(uint32_t)r.y << 32) | (uint32_t)r.x);
-    int64_t tp = __shfl_up_sync(0xffffffffu, t, 1);
-    if (lane == 0 && in) tp = i > 0 ? ev[i - 1].t_us : *prev_t;
-    const uint32_t x = (uint32_t)r.z & 0xffffu, y = (uint32_t)r.z >> 16;
-    const int p = (int)(int8_t)(r.w & 0xff);
-    if (in && ((x >= (uint32_t)W) | (y >= (uint32_t)H) | (p * p != 1) | (t < t_origin) | (t < tp) | (t <= last_frame_t))) {
-      int code;
-      if (x >= (uint32_t)W || y >= (uint32_t)H) code = ESI_ERR_OUT_OF_BOUNDS;
-      else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
-      else code = ESI_ERR_NEGATIVE_INTERVAL;
-      atomicMin(err, ((unsigned long long)i << 8) | (unsigned)code);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U; base < n; base += stride) {
+    int4 r[U];
+    int64_t tp0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * blockDim.x + threadIdx.x;
+      r[u] = i < n ? ld_stream16(evv + i) : make_int4(0, 0, 0, 0);
+      tp0[u] = 0;
+      if (lane == 0 && i < n) tp0[u] = i > 0 ? __ldg(&ev[i - 1].t_us) : *prev_t;
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      validate_one(base + u * blockDim.x + threadIdx.x, n, r[u], tp0[u], lane, t_origin, last_frame_t, W, H, err);
   }
 }
 
@@ -134,8 +151,8 @@ cudaError_t launch_validate(const esi_event_t* ev, int64_t n, const int64_t* pre
                             int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
                             unsigned long long* err, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  int64_t blocks = (n + 1023) / 1024;
+  if (blocks > 148 * 8) blocks = 148 * 8;
   esi_validate_kernel<<<(int)blocks, 256, 0, s>>>(ev, n, prev_t, t_origin, last_frame_t, W, H, err);
   return cudaGetLastError();
 }

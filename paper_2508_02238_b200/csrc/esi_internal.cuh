@@ -44,6 +44,10 @@ constexpr int kMaxBandPx = 4096;
 #define ESI_K2_CTAS 3
 #endif
 constexpr int kK2Ctas = ESI_K2_CTAS;
+#ifndef ESI_K2_WARPS
+#define ESI_K2_WARPS 8
+#endif
+constexpr int kK2Warps = ESI_K2_WARPS;     // warps per fast-K2 CTA
 
 // First error of a render call: (global event index << 8) | code, atomicMin'ed
 // so that the earliest offending event wins (same as the oracle's first error).
@@ -145,10 +149,6 @@ struct IntArgs {
   DecayParams dp;
   MapParams mp;
   WideParams wp;
-  // warp-owned K2 (esi_integrate_warp.cu): warps per CTA, quads per warp,
-  // (q * w2_qmagic) >> 32 == q / w2_qpw, events per sub-batch
-  int32_t w2_nw, w2_qpw, w2_sb;
-  uint32_t w2_qmagic;
   const unsigned long long* gate;    // non-null: exit without writing if *gate != kNoError
 };
 
@@ -182,9 +182,6 @@ cudaError_t launch_plan(const esi_event_t* const* chunk_first, const int64_t* ch
                         int32_t* n_active, cudaStream_t s);
 // fast kernel (32-bit relative times, dt_cut < 2^23) -- esi_integrate_fast.cu
 cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s);
-// warp-owned fast kernel (32-bit relative times, dt_cut < 2^23) -- esi_integrate_warp.cu
-cudaError_t launch_integrate_w2(const IntArgs& a, cudaStream_t s);
-size_t integrate_w2_smem_bytes(int band_px, int n_tiles);
 // consume: for segment k, count events with t <= t_cap (binary search), and set
 // *last_t to the t of the last consumed event of the last segment with one.
 cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,
@@ -201,6 +198,8 @@ cudaError_t launch_route_scatter(const esi_event_t* ev, int64_t n, int32_t H, in
                                  cudaStream_t s);
 int64_t route_tiles(int64_t n);
 cudaError_t launch_fill_i64(int64_t* p, int64_t n, int64_t v, cudaStream_t s);
+cudaError_t launch_frame_metrics(const uint8_t* frames, const float* truth, int64_t P, int n_frames,
+                                 int truth_per_frame, double* pearson, double* mse_norm, cudaStream_t s);
 cudaError_t launch_validate(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
                             int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
                             unsigned long long* err, cudaStream_t s);

@@ -112,10 +112,6 @@ struct esi_handle {
   bool band32 = false;
   bool allow_fast = true;    // K2 fast variant allowed (dt_cut < 2^23)
   bool single_stream = false; // ESI_SINGLE_STREAM=1: K1 and K2 on one stream
-  bool k2_warp = true;        // K2 = warp-owned kernel (esi_integrate_warp.cu); ESI_K2=block: the older
-                              // block-synchronous kernel (esi_integrate_fast.cu), kept for A/B measurements
-  int w2_nw = 1, w2_qpw = 64, w2_sb = 2048;
-  uint32_t w2_qmagic = 0;
 };
 
 namespace {
@@ -367,46 +363,23 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   h->P = P;
   h->prm = prm;
   derive_params(h);
-  // Band size (K1 partition key, K2 CTA).
-  //  * warp-owned K2 (default): 2 CTAs per SM; band_px = ceil(P / (2 * #SMs)) rounded up
-  //    to whole quads (4 px), 128 <= band_px <= kMaxBandPx, <= kMaxBands bands;
-  //    nw = ceil(quads / 64) warps of qpw = ceil(quads / nw) <= 64 quads each (two readout
-  //    steps of 32 lanes x 4 px per warp and frame).  c4: 296 bands of 3116 px, 13 warps.
-  //  * block-synchronous K2 (ESI_K2=block): a multiple of 64 pixels such that the bands fill
-  //    the SMs evenly at kK2Ctas resident 8-warp CTAs per SM (c4: 437 bands of 2112 px).
+  // Band size (K1 partition key, K2 CTA): a multiple of 64 pixels such that
+  // the bands fill the SMs evenly at kK2Ctas resident K2 CTAs (8 warps each) per SM
+  // (c4, 3 per SM: 437 bands of 2112 pixels on 148 SMs), at most kMaxBandPx (shared memory) and at most
+  // kMaxBands bands (K1's shared-memory histograms).
   {
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, prm.device);
-    const char* k2e = getenv("ESI_K2");
-    h->k2_warp = !(k2e && strcmp(k2e, "block") == 0);
-    int64_t bp;
-    if (h->k2_warp) {
-      int ctas = 2;
-      if (const char* e = getenv("ESI_K2_CTAS")) ctas = std::max(1, std::min(4, atoi(e)));
-      const int64_t slots = (int64_t)n_sm * ctas;
-      bp = (P + slots - 1) / slots;
-      bp = ((bp + 3) / 4) * 4;
-      bp = std::max<int64_t>(128, std::min<int64_t>(bp, kMaxBandPx));
-      while ((P + bp - 1) / bp > kMaxBands) bp += 4;
-    } else {
-      const int64_t slots = (int64_t)n_sm * kK2Ctas;
-      bp = (P + slots - 1) / slots;
-      bp = ((bp + 63) / 64) * 64;
-      bp = std::max<int64_t>(64, std::min<int64_t>(bp, kMaxBandPx));
-      while ((P + bp - 1) / bp > kMaxBands) bp += 64;
-    }
+    const int64_t slots = (int64_t)n_sm * kK2Ctas;
+    int64_t bp = (P + slots - 1) / slots;
+    bp = ((bp + 63) / 64) * 64;
+    bp = std::max<int64_t>(64, std::min<int64_t>(bp, kMaxBandPx));
+    while ((P + bp - 1) / bp > kMaxBands) bp += 64;
     if (const char* e = getenv("ESI_BAND_PX")) {
       const int64_t v = atoll(e);
-      const int64_t mult = h->k2_warp ? 4 : 64;
-      if (v >= 64 && v <= kMaxBandPx && v % mult == 0 && (P + v - 1) / v <= kMaxBands) bp = v;
+      if (v >= 64 && v <= kMaxBandPx && v % 64 == 0 && (P + v - 1) / v <= kMaxBands) bp = v;
     }
     h->band_px = (int)bp;
-    const int quads = (int)((bp + 3) / 4);
-    h->w2_nw = (quads + 63) / 64;
-    h->w2_qpw = (quads + h->w2_nw - 1) / h->w2_nw;
-    h->w2_qmagic = (uint32_t)((((uint64_t)1) << 32) / (uint64_t)h->w2_qpw + 1);
-    for (uint32_t q = 0; q < 1024; ++q)   // exactness of the owner division (checked once)
-      if ((uint32_t)(((uint64_t)q * h->w2_qmagic) >> 32) != q / (uint32_t)h->w2_qpw) { delete h; return ESI_ERR_INVALID_ARG; }
   }
   h->nb = (int)((P + h->band_px - 1) / h->band_px);
   h->band_magic = ((uint64_t)1 << 40) / (uint64_t)h->band_px + 1;   // exact pid / band_px for pid < 2^23
@@ -471,9 +444,12 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
       h->atomic_rank = false;
     }
     if (d_bad) cudaFree(d_bad);
-    h->rank_mode = 2;
+    // default: lane-ordered atomics when the probe confirms them (fastest, DESIGN 4), else
+    // peer masks (ordered by construction); ESI_RANK_MODE=peers|ballot|atomic overrides
+    h->rank_mode = h->atomic_rank ? 1 : 2;
+    if (mode && strcmp(mode, "peers") == 0) h->rank_mode = 2;
     if (mode && strcmp(mode, "ballot") == 0) h->rank_mode = 0;
-    if (mode && strcmp(mode, "atomic") == 0 && h->atomic_rank) h->rank_mode = 1;
+    if (mode && strcmp(mode, "atomic") == 0) h->rank_mode = h->atomic_rank ? 1 : 2;
   }
   if (!rc && cudaStreamSynchronize(h->stream) != cudaSuccess) rc = ESI_ERR_CUDA;
   if (rc) {
@@ -791,15 +767,11 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       ia.dp = h->dp;
       ia.mp = h->mp;
       ia.wp = h->wp;
-      ia.w2_nw = h->w2_nw;
-      ia.w2_qpw = h->w2_qpw;
-      ia.w2_sb = h->w2_sb;
-      ia.w2_qmagic = h->w2_qmagic;
       ia.gate = lazy ? h->d_err : nullptr;   // a K1 error so far: K2 exits (frames unspecified, S/T restored)
       TimedLaunch t2;
       timed_begin(h, 1, &t2);
       if (hinfo[c].fast) {
-        ESI_CUDA(h, h->k2_warp ? launch_integrate_w2(ia, st) : launch_integrate_fast(ia, st));
+        ESI_CUDA(h, launch_integrate_fast(ia, st));
         h->st_fast += 1;
       } else {
         ESI_CUDA(h, launch_integrate(ia, st));
@@ -906,7 +878,7 @@ int esi_layout(esi_handle_t* h, int32_t* n_bands, int32_t* band_px, int32_t* war
   if (!h) return ESI_ERR_INVALID_ARG;
   if (n_bands) *n_bands = h->nb;
   if (band_px) *band_px = h->band_px;
-  if (warps_per_band) *warps_per_band = h->k2_warp ? h->w2_nw : 8;
+  if (warps_per_band) *warps_per_band = kK2Warps;
   return ESI_OK;
 }
 
@@ -1078,6 +1050,28 @@ int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t
   }
   if (herr != kNoError) rc = (int)(herr & 0xff);
   return rc;
+}
+
+int esi_frame_metrics(int32_t device, const uint8_t* frames, const float* truth, int64_t n_pixels,
+                      int32_t n_frames, int32_t truth_per_frame, double* pearson, double* mse_norm,
+                      void* stream) {
+  if (!frames || !truth || !pearson || !mse_norm || n_pixels < 1 || n_frames < 0) return ESI_ERR_INVALID_ARG;
+  if (n_frames == 0) return ESI_OK;
+  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return ESI_ERR_INVALID_ARG; }
+  if (!is_device_ptr(frames) || !is_device_ptr(truth)) return ESI_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* d = nullptr;
+  if (cudaMallocAsync((void**)&d, 2 * (size_t)n_frames * sizeof(double), st) != cudaSuccess) {
+    cudaGetLastError();
+    return ESI_ERR_OOM;
+  }
+  cudaError_t e = launch_frame_metrics(frames, truth, n_pixels, n_frames, truth_per_frame, d, d + n_frames, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(pearson, d, n_frames * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(mse_norm, d + n_frames, n_frames * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) { cudaGetLastError(); return ESI_ERR_CUDA; }
+  return ESI_OK;
 }
 
 // ---- device buffers shared between processes (CUDA IPC) for the P2P exchange

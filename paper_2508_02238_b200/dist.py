@@ -328,8 +328,12 @@ class RowBandSharded:
             e1.record()
         full_h = self.bh * self.world
         direct = out is not None and full_h == self.H and out.is_contiguous()
-        buf = out if direct else torch.empty((F, full_h, self.W), dtype=torch.uint8, device=self.device)
-        self._assemble(band, buf)
+        if self.world == 1 and direct:                       # one band = the whole frame: no assembly
+            out.copy_(band)
+            buf = out
+        else:
+            buf = out if direct else torch.empty((F, full_h, self.W), dtype=torch.uint8, device=self.device)
+            self._assemble(band, buf)
         if timing:
             e2.record()
             e2.synchronize()

@@ -79,6 +79,8 @@ def _lib():
         L.esi_enable_kernel_timing.argtypes = [vp, ctypes.c_int]
         L.esi_kernel_time.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.esi_last_render_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.esi_frame_metrics.argtypes = [i32, vp, vp, i64, i32, i32, vp, vp, vp]
+        L.esi_frame_metrics.restype = ctypes.c_int
         L.esi_layout.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
         L.esi_debug_partition.argtypes = [vp, vp, vp, vp, sz, vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
         L.esi_router_create.argtypes = [i32, i32, vp, i32, ctypes.POINTER(vp)]
@@ -189,6 +191,22 @@ def get_error(h: int) -> int:
 
 def destroy(h: int) -> None:
     _lib().esi_destroy(h)
+
+
+def frame_metrics(frames, truth, device: int = 0):
+    """SPEC metrics on the GPU (esi_frame_metrics): frames [F, H, W]
+    uint8 and truth [H, W] or [F, H, W] float32 log intensity, both CUDA tensors.
+    Returns (pearson[F], mse_norm[F]) as numpy float64 (NaN = missing)."""
+    import torch
+    F = frames.shape[0]
+    P = frames[0].numel()
+    per = 1 if truth.dim() == 3 else 0
+    pr = np.empty(F, np.float64)
+    mn = np.empty(F, np.float64)
+    stream = torch.cuda.current_stream(frames.device).cuda_stream
+    _check(_lib().esi_frame_metrics(int(device), _addr(frames.contiguous()), _addr(truth.contiguous()), int(P), int(F),
+                                    per, pr.ctypes.data, mn.ctypes.data, stream), "esi_frame_metrics")
+    return pr, mn
 
 
 class Esi:

@@ -1,0 +1,151 @@
+"""SURVEY 8(f) item 3 on the CUDA path: the naive Eq. 2 integrator against ESI
+on the Fig. 4 noise pathology (SPEC acceptance 4), the Fig. 2 qualitative
+acceptance (SPEC acceptance 3) on the CUDA simulator's ramp + circle scene, and
+the frame-vs-ground-truth scores (SPEC metrics) against their numpy definition.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle.metrics import score_frame
+from esi_synth import from_numpy_struct
+from test_oracle_pins import _noise_stream
+
+pytestmark = pytest.mark.gpu
+
+
+def _pack(a):
+    b = np.zeros(len(a), dtype=[("t", "<i8"), ("x", "<u2"), ("y", "<u2"), ("p", "i1"), ("_pad", "u1", (3,))])
+    for k in ("t", "x", "y", "p"):
+        b[k] = a[k]
+    return from_numpy_struct(b).cuda()
+
+
+def _state(W, H, ev, t_end, **params):
+    from paper_2508_02238_b200 import Esi
+    e = Esi(W, H, **params)
+    try:
+        assert e.push(ev) == 0
+        e.render_many([t_end], torch.empty((1, H, W), dtype=torch.uint8, device="cuda"))
+        return e.get_state()[0]
+    finally:
+        e.close()
+
+
+def test_fig4_noise_pathology_on_gpu():
+    """SPEC acceptance 4: naive Eq. 2 integrator (decay_kind 2) vs
+    ESI on a 2 s pure-noise stream with a 10 kHz hot pixel: the naive 99th
+    percentile |S| exceeds ESI's pre-clamp one (state_unclamped) by >= 5x; ESI's
+    clamped state stays in [s_min, s_max]; both GPU states match the oracle."""
+    W = H = 128
+    a = _noise_stream(4000)
+    ev = _pack(a)
+    S_naive = _state(W, H, ev, 2_000_000, decay_kind=2)
+    S_pre = _state(W, H, ev, 2_000_000, state_unclamped=1)
+    S_esi = _state(W, H, ev, 2_000_000)
+    fac = np.percentile(np.abs(S_naive), 99) / np.percentile(np.abs(S_pre), 99)
+    assert fac >= 5.0, fac
+    assert S_esi.min() >= -1.5 and S_esi.max() <= 1.5
+    _, S_ref, _ = oracle.run(W, H, a, [2_000_000], decay_kind=2)
+    assert np.max(np.abs(S_naive - S_ref)) <= 1e-5 * max(1.0, np.abs(S_ref).max())
+    _, S_ref, _ = oracle.run(W, H, a, [2_000_000])
+    assert np.max(np.abs(S_esi - S_ref)) <= 1e-5
+
+
+def _fig2_run(k=10.0):
+    """The Fig. 2 scene (SPEC defaults: 128x128, c = 0.15, radius 18 px,
+    velocity -60 px/s, 0.5 s stationary lead, 2.5 s) through the CUDA simulator,
+    then ESI (C = c, k, b = 2, bounds -+1.5) at 100 FPS on the GPU."""
+    from esi_synth.cuda_sim import CudaSim, circle_scene
+    from paper_2508_02238_b200 import Esi
+    W = H = 128
+    c = 0.15
+    sc = circle_scene(W, H, c)
+    steps = np.arange(0, 2_500_001, 500, dtype=np.int64)
+    x0, lead, v = 0.75 * W, 0.5, -60.0
+    ts = steps * 1e-6
+    cx = np.where(ts < lead, x0, x0 + v * (ts - lead)).astype(np.float32)
+    sim = CudaSim()
+    t, x, y, p = sim.simulate(sc, steps, cx)
+    from esi_synth import pack_events
+    ev = pack_events(t, x, y, p)
+    tf = np.arange(1, 251, dtype=np.int64) * 10_000
+    e = Esi(W, H, C=c, k=k, b=2.0, s_min=-1.5, s_max=1.5)
+    try:
+        assert e.push(ev) == 0
+        out = torch.empty((len(tf), H, W), dtype=torch.uint8, device="cuda")
+        e.render_many(tf, out)
+    finally:
+        e.close()
+    truth = torch.stack([sim.field(sc, float(np.interp(tj, steps, cx))) for tj in tf])
+    return out, truth, t, tf, (x0, lead, v, sc.radius, H / 2)
+
+
+def _disk(cx, cy, r, W=128, H=128):
+    yy, xx = np.mgrid[0:H, 0:W] + 0.5
+    return (xx - cx) ** 2 + (yy - cy) ** 2 <= r * r
+
+
+def test_fig2_qualitative_acceptance():
+    """SPEC acceptance 3 (Fig. 2): (a) during the
+    stationary lead no event fires and every frame is uniform mid-gray
+    ("the estimated intensity appears uniform"); (b) during the motion the
+    circle region differs from the background (here: the leading crescent, which
+    the darker circle has just covered, vs the static background) by >= 20 gray
+    levels; (c) the reverse-intensity ghost at the circle's initial position
+    decays to within 5 gray levels of the background within 3/k s after the
+    circle has left it."""
+    k = 10.0
+    out, truth, t, tf, (x0, lead, v, r, cy) = _fig2_run(k)
+    f = out.cpu().numpy().astype(np.float64)
+    # (a)
+    assert int(t.min()) >= int(lead * 1e6)
+    for j in np.nonzero(tf < lead * 1e6)[0]:
+        assert (f[j] == 128).all()
+    # (b) frame at 1.5 s: circle centre x(t); leading crescent = inside now, outside 1/k s ago
+    j = int(np.searchsorted(tf, 1_500_000))
+    cxt = x0 + v * (tf[j] * 1e-6 - lead)
+    inside = _disk(cxt, cy, r)
+    was = _disk(cxt - v * (1 / k), cy, r)
+    crescent = inside & ~was
+    background = ~_disk(cxt, cy, r + 8) & ~_disk(cxt - v * 0.5, cy, r + 8)
+    diff = f[j][background].mean() - f[j][crescent].mean()
+    assert diff >= 20.0, diff
+    assert abs(f[j][background].mean() - 128.0) <= 1.0          # static ramp: no events
+    # (c) the circle leaves its initial disk at t_leave; 3/k s later the initial
+    # region (minus anything the circle still covers) is within 5 levels of background
+    t_leave = lead + (2 * r) / (-v)
+    jc = int(np.searchsorted(tf, (t_leave + 3 / k) * 1e6))
+    cxt = x0 + v * (tf[jc] * 1e-6 - lead)
+    ghost = _disk(x0, cy, r) & ~_disk(cxt, cy, r + 8)
+    bg = ~_disk(cxt, cy, r + 8) & ~_disk(x0, cy, r + 8)
+    assert abs(f[jc][ghost].mean() - f[jc][bg].mean()) <= 5.0
+    # ... while right after the circle left, the ghost was visible
+    jl = int(np.searchsorted(tf, t_leave * 1e6))
+    assert abs(f[jl][_disk(x0, cy, r) & ~_disk(x0 + v * (tf[jl] * 1e-6 - lead), cy, r + 8)].mean() - 128.0) >= 5.0
+
+
+def test_frame_metrics_kernel_matches_definition():
+    """esi_frame_metrics (CUDA) against oracle.metrics.score_frame on the Fig. 2
+    frames and ground truth, plus the SPEC examples (affine -> 1, negated -> -1,
+    constant -> missing)."""
+    from paper_2508_02238_b200.esi import frame_metrics
+    out, truth, _, tf, _ = _fig2_run()
+    pr, mn = frame_metrics(out, truth)
+    f = out.cpu().numpy()
+    g = truth.cpu().numpy()
+    for j in range(len(tf)):
+        r, m = score_frame(f[j], g[j])
+        if np.isnan(r):
+            assert np.isnan(pr[j]) and np.isnan(mn[j])
+        else:
+            assert abs(pr[j] - r) <= 1e-9 and abs(mn[j] - m) <= 1e-8
+    assert np.isnan(pr[0])                                   # uniform frame during the stationary lead
+    # a frame that is an affine image of its truth scores 1 (up to 8-bit rounding)
+    g0 = truth[100]
+    fr = ((g0 - g0.min()) / (g0.max() - g0.min()) * 255).round().to(torch.uint8)[None]
+    p1, _ = frame_metrics(fr.contiguous(), g0)
+    assert p1[0] > 0.999
+    p2, m2 = frame_metrics((255 - fr).contiguous(), g0)
+    assert p2[0] < -0.999 and m2[0] > 3.99

@@ -496,7 +496,7 @@ def test_2560x1440_sensor_full_frames():
     e = Esi(w.W, w.H, **w.params)
     try:
         nb, bp, nw = e.layout()
-        assert bp == 4096 and nb == 900 and nw == 16
+        assert bp == 4096 and nb == 900 and nw == 8
     finally:
         e.close()
     _prefix_check(w, 500_000, 100)

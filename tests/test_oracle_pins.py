@@ -624,3 +624,66 @@ def test_eq14_ties_through_the_render_path():
         o = Oracle(1, 1, s_min=c["lo"], s_max=c["hi"], readout_decay=0)
         o.set_state(np.array([c["v"]]), np.array([0]))
         assert o.render(10)[0, 0] == c["expect"], c
+
+
+# ---------------------------------------------------------------- SPEC metrics, f3
+def test_metrics_pins():
+    """SPEC score_frame examples and the affine-invariance property
+    (S:425): recon = a x + b (a > 0) -> pearson 1, mse_norm 0; negated -> -1, 4;
+    uniform recon -> missing; mse_norm = 2 (1 - pearson) for any pair."""
+    from oracle.metrics import score_frame, score_run
+    rng = np.random.default_rng(401)
+    truth = rng.normal(size=(24, 32))
+    for _ in range(20):
+        a, b = rng.uniform(0.01, 50), rng.uniform(-100, 100)
+        r, m = score_frame(a * truth + b, truth)
+        assert abs(r - 1.0) <= 1e-9 and abs(m) <= 1e-9
+        r, m = score_frame(-a * truth + b, truth)
+        assert abs(r + 1.0) <= 1e-9 and abs(m - 4.0) <= 1e-8
+    r, m = score_frame(np.full((24, 32), 128), truth)
+    assert np.isnan(r) and np.isnan(m)
+    x = rng.normal(size=(24, 32))
+    r, m = score_frame(x, truth)
+    assert abs(m - 2 * (1 - r)) <= 1e-12
+    assert abs(r - np.corrcoef(x.ravel(), truth.ravel())[0, 1]) <= 1e-12    # textbook definition
+    sc, summ = score_run([x, np.zeros((24, 32)), truth], [truth] * 3)
+    assert summ["missing"] == 1 and abs(summ["min"] - r) <= 1e-12
+    assert abs(summ["mean"] - (r + 1.0) / 2) <= 1e-12
+
+
+# ---------------------------------------------------------------- SPEC acceptance 4 (S:535), Fig. 4
+def _noise_stream(seed, W=128, H=128, rate=5.0, dur_us=2_000_000, hot=(64, 64), hot_hz=10_000.0):
+    """SPEC acceptance 4: a 2 s pure-noise stream, background 5 ev/px/s (Poisson,
+    random polarity), one hot pixel at 10 kHz (Fig. 3: noise events and a hot
+    pixel, P:104)."""
+    rng = np.random.default_rng(seed)
+    n_bg = rng.poisson(rate * W * H * dur_us * 1e-6)
+    n_hot = rng.poisson(hot_hz * dur_us * 1e-6)
+    t = np.concatenate([rng.integers(0, dur_us, n_bg), rng.integers(0, dur_us, n_hot)])
+    x = np.concatenate([rng.integers(0, W, n_bg), np.full(n_hot, hot[0])])
+    y = np.concatenate([rng.integers(0, H, n_bg), np.full(n_hot, hot[1])])
+    p = rng.choice(np.array([-1, 1], np.int8), n_bg + n_hot)
+    o = np.argsort(t, kind="stable")
+    a = np.zeros(len(t), dtype=[("t", "<i8"), ("x", "<u2"), ("y", "<u2"), ("p", "i1")])
+    a["t"], a["x"], a["y"], a["p"] = t[o], x[o], y[o], p[o]
+    return a
+
+
+def test_fig4_noise_pathology_factor_oracle():
+    """SPEC acceptance 4 (Fig. 4 'severe noise will quickly
+    destroy the estimated intensity'): on the pure-noise stream the naive Eq. 2
+    integrator's 99th-percentile |S| exceeds ESI's (pre-clamp: the per-event
+    clamp removed) by a factor >= 5, and ESI's clamped state stays inside
+    [s_min, s_max].  Monte-Carlo confirmation of the constant: the
+    factor on five seeds is printed by the assertion message."""
+    W = H = 128
+    tf = [2_000_000]
+    facs = []
+    for seed in range(5):
+        a = _noise_stream(4000 + seed)
+        _, S_naive, _ = oracle.run(W, H, a, tf, decay_kind=2)
+        _, S_pre, _ = oracle.run(W, H, a, tf, state_unclamped=1)
+        _, S_esi, _ = oracle.run(W, H, a, tf)
+        facs.append(np.percentile(np.abs(S_naive), 99) / np.percentile(np.abs(S_pre), 99))
+        assert S_esi.min() >= -1.5 and S_esi.max() <= 1.5
+    assert min(facs) >= 5.0, facs
