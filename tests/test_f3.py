@@ -121,9 +121,15 @@ def test_fig2_qualitative_acceptance():
     ghost = _disk(x0, cy, r) & ~_disk(cxt, cy, r + 8)
     bg = ~_disk(cxt, cy, r + 8) & ~_disk(x0, cy, r + 8)
     assert abs(f[jc][ghost].mean() - f[jc][bg].mean()) <= 5.0
-    # ... while right after the circle left, the ghost was visible
-    jl = int(np.searchsorted(tf, t_leave * 1e6))
-    assert abs(f[jl][_disk(x0, cy, r) & ~_disk(x0 + v * (tf[jl] * 1e-6 - lead), cy, r + 8)].mean() - 128.0) >= 5.0
+    # ... while the ghost is visible right behind the moving circle: pixels its trailing
+    # edge passed 10-50 ms ago (inside the disk at t - 0.05 s, outside it with a 1 px
+    # margin at t - 0.01 s) saw ON events (the 30 % circle left: brighter) and have
+    # decayed by at most (1 - k 0.05)^2 = 1/4 -- reverse intensity, above mid-gray
+    jl = int(np.searchsorted(tf, (lead + 0.3) * 1e6))
+    c_at = lambda s: x0 + v * (tf[jl] * 1e-6 - s - lead)
+    trail = _disk(c_at(0.05), cy, r) & ~_disk(c_at(0.01), cy, r + 1)
+    assert trail.sum() > 20
+    assert f[jl][trail].mean() - 128.0 >= 5.0, f[jl][trail].mean()
 
 
 def test_frame_metrics_kernel_matches_definition():
