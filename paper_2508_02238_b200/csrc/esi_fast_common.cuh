@@ -193,3 +193,75 @@ __device__ __forceinline__ int upper_bound_rel(const uint2* sub, int n, uint32_t
   return lo + 1;
 }
 
+
+// Where the band's events of the chunk are: K1 wrote, per tile t, the band's run
+// at rec[t * kTile + mo[t]] with count cnt[t] (meta[t] = mo | cnt << 16).
+// Fills pre[t] = band events before tile t (pre[n_tiles] = total) and mo[t];
+// returns the total.  Block-wide (NW warps), one barrier inside.
+template <int NW>
+__device__ __forceinline__ int band_run_prefix(const uint32_t* __restrict__ meta, int n_tiles, uint32_t* pre,
+                                               uint16_t* mo, uint32_t* s_wsum) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per = (n_tiles + NW * 32 - 1) / (NW * 32);
+  const int t0 = threadIdx.x * per;
+  uint32_t local = 0;
+  for (int t = t0; t < min(n_tiles, t0 + per); ++t) {
+    const uint32_t m = meta[t];
+    mo[t] = (uint16_t)(m & 0xffffu);
+    local += m >> 16;
+  }
+  uint32_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  uint32_t run = x - local, tot = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const uint32_t v = s_wsum[w];
+    if (w < warp) run += v;
+    tot += v;
+  }
+  for (int t = t0; t < min(n_tiles, t0 + per); ++t) {
+    pre[t] = run;
+    run += meta[t] >> 16;
+  }
+  if (threadIdx.x == 0) pre[n_tiles] = tot;
+  return (int)tot;
+}
+
+// Gather band events [sb0, min(sb0 + SB, n_b)) into dst with cp.async: 8 (tile,
+// band) segments per warp step, 4 lanes per segment, tiles in order = arrival order.
+// Warps gw = 0 .. ngw-1 share the copies.
+template <int SB>
+__device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const uint32_t* pre, const uint16_t* mo,
+                                           int n_tiles, int n_b, int sb0, uint2* dst, int gw, int ngw, int lane) {
+  const uint32_t q_end = (uint32_t)min(sb0 + SB, n_b);
+  int t_lo = 0;                                 // last tile with pre[t] <= sb0 (32-ary search)
+#pragma unroll
+  for (int stride = 1024; stride >= 1; stride >>= 5) {
+    const int t = t_lo + lane * stride;
+    const unsigned b = __ballot_sync(kFull, t < n_tiles && pre[t] <= (uint32_t)sb0);
+    t_lo += (31 - __clz(b | 1u)) * stride;
+  }
+  for (int tb = t_lo + gw * 8; tb < n_tiles; tb += ngw * 8) {
+    if (pre[tb] >= q_end) break;                // segments are in order: the rest is later
+    const int t = tb + (lane >> 2);
+    uint32_t i0 = 0, i1 = 0, p0 = 0;
+    const uint2* src = rec;
+    if (t < n_tiles) {
+      p0 = pre[t];
+      if (p0 < q_end) {
+        i0 = p0 < (uint32_t)sb0 ? (uint32_t)sb0 - p0 : 0u;
+        i1 = min(pre[t + 1], q_end) - p0;
+      }
+      src += (size_t)t * kTile + mo[t];
+    }
+    const int dofs = (int)p0 - sb0;             // >= -i0
+    for (uint32_t i = i0 + (lane & 3); i < i1; i += 4) cp_async8(&dst[dofs + (int)i], src + i);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}

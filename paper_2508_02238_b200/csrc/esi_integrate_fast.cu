@@ -247,38 +247,6 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
 }
 
 
-// Gather band events [sb0, min(sb0 + kSB, n_b)) into dst with cp.async: 8 (tile,
-// band) segments per warp step, 4 lanes per segment, tiles in order = arrival order.
-// Warps gw = 0 .. ngw-1 share the copies.
-__device__ __forceinline__ void gather_sub(const uint2* __restrict__ rec, const uint32_t* pre, const uint16_t* mo,
-                                           int n_tiles, int n_b, int sb0, uint2* dst, int gw, int ngw, int lane) {
-  const uint32_t q_end = (uint32_t)min(sb0 + kSB, n_b);
-  int t_lo = 0;                                 // last tile with pre[t] <= sb0 (32-ary search)
-#pragma unroll
-  for (int stride = 1024; stride >= 1; stride >>= 5) {
-    const int t = t_lo + lane * stride;
-    const unsigned b = __ballot_sync(kFull, t < n_tiles && pre[t] <= (uint32_t)sb0);
-    t_lo += (31 - __clz(b | 1u)) * stride;
-  }
-  for (int tb = t_lo + gw * 8; tb < n_tiles; tb += ngw * 8) {
-    if (pre[tb] >= q_end) break;                // segments are in order: the rest is later
-    const int t = tb + (lane >> 2);
-    uint32_t i0 = 0, i1 = 0, p0 = 0;
-    const uint2* src = rec;
-    if (t < n_tiles) {
-      p0 = pre[t];
-      if (p0 < q_end) {
-        i0 = p0 < (uint32_t)sb0 ? (uint32_t)sb0 - p0 : 0u;
-        i1 = min(pre[t + 1], q_end) - p0;
-      }
-      src += (size_t)t * kTile + mo[t];
-    }
-    const int dofs = (int)p0 - sb0;             // >= -i0
-    for (uint32_t i = i0 + (lane & 3); i < i1; i += 4) cp_async8(&dst[dofs + (int)i], src + i);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
 template <int BM>
 __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -309,46 +277,14 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
     sm.head[i] = 0u;                          // generation 0: never a live claim
   }
   if (threadIdx.x == 0) *sm.nd = 0;
-  int n_b = 0;
-  if (active) {
-    const uint32_t* meta = a.meta + (int64_t)band * n_tiles;
-    const int per = (n_tiles + kNT - 1) / kNT;
-    const int t0 = threadIdx.x * per;
-    uint32_t local = 0;
-    for (int t = t0; t < min(n_tiles, t0 + per); ++t) {
-      const uint32_t m = meta[t];
-      sm.mo[t] = (uint16_t)(m & 0xffffu);
-      local += m >> 16;
-    }
-    uint32_t x = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_wsum[warp] = x;
-    __syncthreads();
-    uint32_t run = x - local, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kNW; ++w) {
-      const uint32_t v = s_wsum[w];
-      if (w < warp) run += v;
-      tot += v;
-    }
-    for (int t = t0; t < min(n_tiles, t0 + per); ++t) {
-      sm.pre[t] = run;
-      run += meta[t] >> 16;
-    }
-    if (threadIdx.x == 0) sm.pre[n_tiles] = tot;
-    n_b = (int)tot;
-  }
+  const int n_b = active ? band_run_prefix<kNW>(a.meta + (int64_t)band * n_tiles, n_tiles, sm.pre, sm.mo, s_wsum) : 0;
   __syncthreads();
 
   int j = f_lo;
   bool done = false;
   uint32_t gen = 0;
   // ---- 1. gather sub-batch k into sub[k & 1]; sub-batch k+1 is in flight while k is integrated
-  if (n_b > 0) gather_sub(a.rec, sm.pre, sm.mo, n_tiles, n_b, 0, sm.sub[0], warp, kNW, lane);
+  if (n_b > 0) gather_sub<kSB>(a.rec, sm.pre, sm.mo, n_tiles, n_b, 0, sm.sub[0], warp, kNW, lane);
   for (int sb0 = 0, kb = 0; sb0 < n_b && !done; sb0 += kSB, ++kb) {
     const int n_sb = min(kSB, n_b - sb0);
     const uint2* sub = (kb & 1) ? sm.sub[1] : sm.sub[0];   // no dynamic index into sm (keeps it in registers)
@@ -356,7 +292,7 @@ __global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) 
     __syncthreads();
     // warp 0 lists the first windows meanwhile (the other warps wait for that list)
     if (sb0 + kSB < n_b && warp > 0)
-      gather_sub(a.rec, sm.pre, sm.mo, n_tiles, n_b, sb0 + kSB, (kb & 1) ? sm.sub[0] : sm.sub[1], warp - 1, kNW - 1,
+      gather_sub<kSB>(a.rec, sm.pre, sm.mo, n_tiles, n_b, sb0 + kSB, (kb & 1) ? sm.sub[0] : sm.sub[1], warp - 1, kNW - 1,
                  lane);
     // ---- 2. segments = frame windows inside the sub-batch; readout at each window end.
     // Window ends (events of the sub-batch with t <= t_j) are listed by warp 0,
