@@ -182,9 +182,6 @@ cudaError_t launch_plan(const esi_event_t* const* chunk_first, const int64_t* ch
                         int32_t* n_active, cudaStream_t s);
 // fast kernel (32-bit relative times, dt_cut < 2^23) -- esi_integrate_fast.cu
 cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s);
-// fast kernel by pixel-grouped passes (the default K2) -- esi_integrate_px.cu
-cudaError_t launch_integrate_px(const IntArgs& a, cudaStream_t s);
-size_t integrate_px_smem_bytes(int band_px, int n_tiles);
 // consume: for segment k, count events with t <= t_cap (binary search), and set
 // *last_t to the t of the last consumed event of the last segment with one.
 cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,

@@ -105,7 +105,6 @@ struct esi_handle {
   std::vector<TimedLaunch> timed;
   std::vector<cudaEvent_t> ev_pool;
   int64_t st_launches = 0, st_events = 0, st_chunks = 0, st_fast = 0;
-  bool k2_claim = false;     // ESI_K2=claim: the per-window claim-chain K2 (esi_integrate_fast.cu)
   bool atomic_rank = true;   // lane-ordered smem atomics observed (probed at create)
   int rank_mode = 2;         // K1 stable ranks: 2 = peer masks (ordered by construction, default),
                              // 1 = lane-ordered atomics (only if probed), 0 = ballot multi-split
@@ -429,8 +428,6 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   // accumulate them in fp64 (wide kernel) rather than fp32
   h->allow_fast = h->dp.dt_cut < ((int64_t)1 << 23) && !h->dp.unclamped && !getenv("ESI_DISABLE_FAST");
   h->single_stream = getenv("ESI_SINGLE_STREAM") && atoi(getenv("ESI_SINGLE_STREAM")) != 0;
-  // K2 of the fast path: pixel-grouped passes (default) or claim chains per frame window (ESI_K2=claim)
-  h->k2_claim = getenv("ESI_K2") && strcmp(getenv("ESI_K2"), "claim") == 0;
   if (!rc) {
     // K1 rank mode: probe that warp-wide smem atomics serve same-address lanes in lane order
     const char* mode = getenv("ESI_RANK_MODE");
@@ -774,7 +771,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       TimedLaunch t2;
       timed_begin(h, 1, &t2);
       if (hinfo[c].fast) {
-        ESI_CUDA(h, h->k2_claim ? launch_integrate_fast(ia, st) : launch_integrate_px(ia, st));
+        ESI_CUDA(h, launch_integrate_fast(ia, st));
         h->st_fast += 1;
       } else {
         ESI_CUDA(h, launch_integrate(ia, st));
