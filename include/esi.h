@@ -236,6 +236,43 @@ int esi_frame_metrics(int32_t device, const uint8_t* frames, const float* truth,
                       int32_t n_frames, int32_t truth_per_frame, double* pearson, double* mse_norm,
                       void* stream);
 
+/* ---- time-sharded single streams ----------------------
+ *
+ * A time slice of the stream acts on one pixel's state (S, T) of Alg. 2
+ * as: no event -> identity; events e_1..e_n ->
+ *   S1 = clamp((S + p_1 C) d(t_1 - T))      (decay-first variant: clamp(S d + p_1 C))
+ *   S' = G(S1),  T' = t_n,
+ * with G = g_n o ... o g_2 the composition of the later events' clamped affine
+ * maps g_k(s) = clamp(d_k s + d_k p_k C, S_min, S_max), d_k = d(t_k - t_{k-1})
+ * (Eq. 4; Eq. 13).  Only the first event's decay sees the
+ * incoming T, so a slice is summarised per pixel by esi_slice_map_t, and the
+ * summaries of consecutive slices compose (B's first event decays from A's
+ * t_last): an exclusive scan of slice maps across GPUs gives every time shard
+ * its incoming state (the Eq. 5 per-pixel product of decays composes).
+ * G is kept in fp32 (the fp32 state tolerance of the render path applies). */
+typedef struct {
+  int64_t t_first;   /* t of the slice's first event at the pixel (us) */
+  int64_t t_last;    /* t of its last event */
+  float a, c, lo, hi;/* G(s) = min(max(a s + c, lo), hi), a >= 0 */
+  int32_t n;         /* events of the slice at the pixel; 0 = identity (other fields unused) */
+  int32_t p_first;   /* polarity of the first event */
+} esi_slice_map_t;   /* 40 bytes */
+
+/* maps [W*H] (DEVICE pointer, overwritten) <- the summary of the n events
+ * (host or device pointer; validated like esi_push_events: sensor bounds,
+ * polarity, non-decreasing t; the first error code is returned and maps are
+ * unspecified).  Uses the handle's parameters and stream; does not touch its
+ * state or pending events.  Chunks of the slice must each span < 2^31 us
+ * (ESI_ERR_INVALID_ARG otherwise).  Synchronises the handle's stream. */
+int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, esi_slice_map_t* maps);
+/* out = `first` followed by `second` (all DEVICE pointers of W*H maps; out may
+ * alias either input).  Stream-ordered on the handle's stream. */
+int esi_slice_compose(esi_handle_t* h, const esi_slice_map_t* first, const esi_slice_map_t* second,
+                      esi_slice_map_t* out);
+/* The handle's state (S, T) <- the action of `maps` (DEVICE pointer).  No event
+ * may be pending (ESI_ERR_INVALID_ARG).  Stream-ordered. */
+int esi_slice_apply(esi_handle_t* h, const esi_slice_map_t* maps);
+
 /* ---- instrumentation (used by bench.py and the parity tests) -------------- */
 
 /* Per-kernel device time accumulated by the handle when timing is enabled

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libesi.so")
-SOURCES = ["esi_partition.cu", "esi_integrate.cu", "esi_integrate_fast.cu", "esi_aux.cu", "esi_metrics.cu", "esi_route.cu", "esi_runtime.cpp"]
+SOURCES = ["esi_partition.cu", "esi_integrate.cu", "esi_integrate_fast.cu", "esi_aux.cu", "esi_metrics.cu", "esi_slice.cu", "esi_route.cu", "esi_runtime.cpp"]
 HEADERS = ["esi_internal.cuh", "esi_device.cuh", "esi_fast_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

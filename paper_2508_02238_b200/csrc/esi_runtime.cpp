@@ -1129,6 +1129,114 @@ int esi_stream_sync(int32_t device, void* stream) {
   return ESI_OK;
 }
 
+int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, esi_slice_map_t* maps) {
+  if (!h || !maps || (n && !events)) return ESI_ERR_INVALID_ARG;
+  if (h->sticky) return h->sticky;
+  cudaSetDevice(h->prm.device);
+  if (!is_device_ptr(maps)) return ESI_ERR_INVALID_ARG;
+  cudaStream_t st = h->stream;
+  ESI_CUDA(h, cudaMemsetAsync(maps, 0, (size_t)h->P * sizeof(esi_slice_map_t), st));   // n = 0: identity
+  if (n == 0) {
+    ESI_CUDA(h, cudaStreamSynchronize(st));
+    return ESI_OK;
+  }
+  const esi_event_t* ev = events;
+  esi_event_t* tmp = nullptr;
+  if (!is_device_ptr(events)) {
+    if (cudaMalloc((void**)&tmp, n * sizeof(esi_event_t)) != cudaSuccess) {
+      cudaGetLastError();
+      return ESI_ERR_OOM;
+    }
+    ESI_CUDA(h, cudaMemcpyAsync(tmp, events, n * sizeof(esi_event_t), cudaMemcpyHostToDevice, st));
+    ev = tmp;
+  }
+  int rc = ESI_OK;
+  int64_t* d_prev = nullptr;
+  auto fail = [&](int code) { rc = code; };
+  if (cudaMalloc((void**)&d_prev, sizeof(int64_t)) != cudaSuccess) { cudaGetLastError(); fail(ESI_ERR_OOM); }
+  // validation (as a push: sensor bounds, polarity, non-decreasing t >= t_origin)
+  if (!rc) {
+    cudaError_t e = launch_fill_i64(d_prev, 1, INT64_MIN, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = launch_validate(ev, (int64_t)n, d_prev, h->prm.t_origin_us, INT64_MIN, h->W, h->H, h->d_err, st);
+    unsigned long long herr = kNoError;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, h->d_err, sizeof(herr), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) fail(cuda_fail(h, e));
+    else if (herr != kNoError) fail((int)(herr & 0xff));
+  }
+  for (int64_t o = 0; !rc && o < (int64_t)n; o += h->chunk_events) {
+    const int64_t nc = std::min<int64_t>(h->chunk_events, (int64_t)n - o);
+    int64_t t01[2];
+    cudaError_t e = cudaMemcpyAsync(&t01[0], &ev[o].t_us, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&t01[1], &ev[o + nc - 1].t_us, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { fail(cuda_fail(h, e)); break; }
+    if (t01[1] - t01[0] >= ((int64_t)1 << 31)) { fail(ESI_ERR_INVALID_ARG); break; }
+    const int n_tiles = (int)((nc + kTile - 1) / kTile);
+    PartArgs pa;
+    pa.ev = ev + o;
+    pa.n = nc;
+    pa.index_base = o;
+    pa.prev_t = d_prev;
+    pa.t_origin = h->prm.t_origin_us;
+    pa.last_frame_t = INT64_MIN;
+    pa.t_min = h->prm.t_origin_us;
+    pa.t_cap = INT64_MAX;
+    pa.W = h->W;
+    pa.H = h->H;
+    pa.band_px = h->band_px;
+    pa.nb = h->nb;
+    pa.band_magic = h->band_magic;
+    pa.band_magic32 = h->band_magic32;
+    pa.band32 = h->band32 ? 1 : 0;
+    pa.validate = 0;   // validated above
+    pa.rec = h->rec[0];
+    pa.meta = h->meta[0];
+    pa.tile_t0 = h->tile_t0[0];
+    pa.tile_wide = h->tile_wide[0];
+    pa.wide_t = h->wide_t[0];
+    pa.err = h->d_err;
+    IntArgs ia{};
+    ia.rec = h->rec[0];
+    ia.meta = h->meta[0];
+    ia.n_tiles = n_tiles;
+    ia.P = h->P;
+    ia.band_px = h->band_px;
+    ia.nb = h->nb;
+    ia.dp = h->dp;
+    ia.mp = h->mp;
+    e = launch_partition(pa, n_tiles, h->rank_mode, st);
+    if (e == cudaSuccess) e = launch_slice_summary(ia, t01[0], maps, st);
+    if (e != cudaSuccess) fail(cuda_fail(h, e));
+  }
+  if (!rc) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(h, e);
+  }
+  if (d_prev) cudaFree(d_prev);
+  if (tmp) cudaFree(tmp);
+  return rc;
+}
+
+int esi_slice_compose(esi_handle_t* h, const esi_slice_map_t* first, const esi_slice_map_t* second,
+                      esi_slice_map_t* out) {
+  if (!h || !first || !second || !out) return ESI_ERR_INVALID_ARG;
+  if (h->sticky) return h->sticky;
+  cudaSetDevice(h->prm.device);
+  ESI_CUDA(h, launch_slice_compose(first, second, out, h->P, h->dp, h->mp, h->stream));
+  return ESI_OK;
+}
+
+int esi_slice_apply(esi_handle_t* h, const esi_slice_map_t* maps) {
+  if (!h || !maps) return ESI_ERR_INVALID_ARG;
+  if (h->sticky) return h->sticky;
+  if (!h->segs.empty()) return ESI_ERR_INVALID_ARG;
+  cudaSetDevice(h->prm.device);
+  ESI_CUDA(h, launch_slice_apply(maps, h->dS, h->dT, h->P, h->dp, h->mp, h->stream));
+  return ESI_OK;
+}
+
 int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8_t* out_p,
                         size_t n_out, uint32_t* band_start, int32_t* nb_out, int32_t* band_px_out) {
   if (!h || !band_start || !nb_out || !band_px_out) return ESI_ERR_INVALID_ARG;

@@ -396,3 +396,74 @@ class StreamSharded:
             if hasattr(h, "close"):
                 h.close()
         self.handles = {}
+
+
+def time_slices(t_events: np.ndarray, t_frames: np.ndarray, world: int):
+    """Split one stream in time for `world` ranks: rank r
+    renders frames [F r / G, F (r+1) / G) and integrates the events with
+    t in (b_r, b_{r+1}], b_r = the last frame time of rank r-1 (events at a frame
+    time belong to that frame, reading A6).  Returns (event bounds, frame bounds)."""
+    F = len(t_frames)
+    fb = [F * r // world for r in range(world + 1)]
+    eb = [0]
+    for r in range(1, world):
+        b = int(t_frames[fb[r] - 1]) if fb[r] > 0 else np.iinfo(np.int64).min
+        eb.append(int(np.searchsorted(t_events, b, side="right")))
+    eb.append(len(t_events))
+    return eb, fb
+
+
+class TimeSharded:
+    """one stream sharded in time (rank order = time order).
+
+    A time slice acts on each pixel's state through the first event's decay
+    (which sees the incoming T) followed by one clamped affine map (the Eq. 5
+    product of decays composes; esi.h ``esi_slice_map_t``), so:
+      1. every rank summarises its slice (``esi_slice_summarize``, P x 40 B);
+      2. the summaries are all-gathered (one collective; NCCL over NVLink);
+      3. rank r composes the summaries of ranks < r (the exclusive scan,
+         ``esi_slice_compose``) and applies it to the initial state
+         (``esi_slice_apply``): its slice's incoming state;
+      4. rank r integrates its slice and renders its frames.
+    The handle is injectable (``handle_factory``) so the orchestration runs in
+    the gloo CPU tests with an oracle-backed stand-in; the product path uses
+    libesi handles (all arithmetic in its kernels)."""
+
+    def __init__(self, width: int, height: int, group=None, handle_factory: Optional[Callable] = None, **params):
+        if handle_factory is None:
+            from .esi import Esi as handle_factory
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.h = handle_factory(width, height, **params)
+        self.timing = {}
+
+    def close(self):
+        if self.h is not None:
+            self.h.close()
+            self.h = None
+
+    def incoming_state_maps(self, events_slice):
+        """Steps 1-3: the exclusive prefix of the slices' maps (None on rank 0)."""
+        maps = self.h.slice_summarize(events_slice)
+        gathered = [torch.empty_like(maps) for _ in range(self.world)]
+        dist.all_gather(gathered, maps, group=self.group)
+        if self.rank == 0:
+            return None
+        pre = gathered[0]
+        for s in range(1, self.rank):
+            pre = self.h.slice_compose(pre, gathered[s])
+        return pre
+
+    def run(self, events_slice, t_frames_slice, out=None):
+        pre = self.incoming_state_maps(events_slice)
+        self.h.reset()
+        if pre is not None:
+            self.h.slice_apply(pre)
+        rc = self.h.push(events_slice)
+        if rc != 0:
+            raise RuntimeError(f"push of the time slice failed (status {rc})")
+        return self.h.render_many(t_frames_slice, out)
+
+    def get_state(self):
+        return self.h.get_state()

@@ -29,6 +29,11 @@ ESI_ERR_NEGATIVE_INTERVAL = 4
 ESI_ERR_CUDA = 5
 ESI_ERR_OOM = 6
 
+# per-pixel summary of a time slice (esi_slice_map_t)
+SLICE_MAP_DTYPE = np.dtype([("t_first", "<i8"), ("t_last", "<i8"), ("a", "<f4"), ("c", "<f4"), ("lo", "<f4"),
+                            ("hi", "<f4"), ("n", "<i4"), ("p_first", "<i4")])
+assert SLICE_MAP_DTYPE.itemsize == 40
+
 # 16-byte packed event record (esi_event_t; SPEC S:370 layout)
 EVENT_DTYPE = np.dtype([("t", "<i8"), ("x", "<u2"), ("y", "<u2"), ("p", "i1"), ("_pad", "u1", (3,))])
 assert EVENT_DTYPE.itemsize == 16
@@ -94,6 +99,9 @@ def _lib():
         L.esi_ipc_open.argtypes = [i32, vp, ctypes.POINTER(vp)]
         L.esi_ipc_close.argtypes = [i32, vp]
         L.esi_stream_sync.argtypes = [i32, vp]
+        L.esi_slice_summarize.argtypes = [vp, vp, sz, vp]
+        L.esi_slice_compose.argtypes = [vp, vp, vp, vp]
+        L.esi_slice_apply.argtypes = [vp, vp]
         for f in ("esi_router_create", "esi_router_count", "esi_router_scatter", "esi_route_bands",
                   "esi_buffer_alloc", "esi_buffer_free", "esi_ipc_get_handle", "esi_ipc_open",
                   "esi_ipc_close", "esi_stream_sync"):
@@ -101,7 +109,8 @@ def _lib():
         for f in ("esi_create", "esi_push_events", "esi_render", "esi_render_many", "esi_get_state",
                   "esi_set_state", "esi_reset", "esi_set_stream", "esi_get_error",
                   "esi_enable_kernel_timing", "esi_kernel_time", "esi_last_render_stats",
-                  "esi_debug_partition", "esi_layout"):
+                  "esi_debug_partition", "esi_layout", "esi_slice_summarize", "esi_slice_compose",
+                  "esi_slice_apply"):
             getattr(L, f).restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -317,6 +326,30 @@ class Esi:
         a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         _check(_lib().esi_layout(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "esi_layout")
         return a.value, b.value, c.value
+
+    # ---- time-sharded streams (esi_slice_*): maps are CUDA uint8 tensors of P x 40 bytes
+    def slice_maps_empty(self):
+        import torch
+        return torch.zeros((self.P, SLICE_MAP_DTYPE.itemsize), dtype=torch.uint8,
+                           device=torch.device("cuda", self.params.device))
+
+    def slice_summarize(self, events, out=None):
+        """Per-pixel summary (esi_slice_map_t) of a time slice of events."""
+        out = self.slice_maps_empty() if out is None else out
+        n = _nbytes(events) // 16
+        _check(_lib().esi_slice_summarize(self.h, _addr(events) if n else None, int(n), _addr(out)),
+               "esi_slice_summarize")
+        return out
+
+    def slice_compose(self, first, second, out=None):
+        """`first` followed by `second` (stream-ordered on the handle's stream)."""
+        out = self.slice_maps_empty() if out is None else out
+        _check(_lib().esi_slice_compose(self.h, _addr(first), _addr(second), _addr(out)), "esi_slice_compose")
+        return out
+
+    def slice_apply(self, maps):
+        """The handle's state <- the action of `maps` (no event may be pending)."""
+        _check(_lib().esi_slice_apply(self.h, _addr(maps)), "esi_slice_apply")
 
     def debug_partition(self, n_max: int):
         t = np.empty(n_max, np.int64)
