@@ -12,9 +12,21 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <optional>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "esi_internal.cuh"
+
+// NVTX ranges around the ABI calls and the render phases (header-only NVTX v3:
+// no-ops unless a profiler is attached), so timelines show the host-side phases.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace esi {
 cudaError_t launch_fill_i64(int64_t* p, int64_t n, int64_t v, cudaStream_t s);
@@ -495,6 +507,7 @@ void esi_destroy(esi_handle_t* h) {
 }
 
 int esi_reset(esi_handle_t* h) {
+  NvtxRange nvtx_range_("esi_reset");
   if (!h) return ESI_ERR_INVALID_ARG;
   cudaSetDevice(h->prm.device);
   cudaStreamSynchronize(h->stream);
@@ -525,6 +538,7 @@ int esi_get_error(esi_handle_t* h) {
 }
 
 int esi_push_events(esi_handle_t* h, const esi_event_t* events, size_t n) {
+  NvtxRange nvtx_range_("esi_push_events");
   if (!h) return ESI_ERR_INVALID_ARG;
   if (h->sticky) return h->sticky;
   if (n == 0) return ESI_OK;
@@ -575,6 +589,7 @@ int esi_push_events(esi_handle_t* h, const esi_event_t* events, size_t n) {
 }
 
 int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) {
+  NvtxRange nvtx_range_("esi_render_many");
   if (!h) return ESI_ERR_INVALID_ARG;
   if (h->sticky) return h->sticky;
   if (F == 0) return ESI_OK;
@@ -671,6 +686,8 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_first, hcf, nc * sizeof(void*), cudaMemcpyHostToDevice, st));
     ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_n, hcn, nc * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     h->st_launches += 1;   // plan
+    std::optional<NvtxRange> plan_range;
+    plan_range.emplace("render: plan (+ host read-back)");
     ESI_CUDA(h, launch_plan(h->d_chunk_first, h->d_chunk_n, (int)nc, h->d_tf, (int)F, t_cap,
                             h->allow_fast ? 1 : 0, h->d_info, h->d_n_active, st));
     int32_t* hna = (int32_t*)(h->h_pin + nc * 16 + 16);
@@ -678,6 +695,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     std::vector<ChunkInfo> hinfo(nc);
     ESI_CUDA(h, cudaMemcpyAsync(hinfo.data(), h->d_info, nc * sizeof(ChunkInfo), cudaMemcpyDeviceToHost, st));
     ESI_CUDA(h, cudaStreamSynchronize(st));
+    plan_range.reset();
     const int n_act = std::max(1, *hna);
     ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
     const bool lazy = !h->prm.validate_on_push;
@@ -838,10 +856,12 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
 }
 
 int esi_render(esi_handle_t* h, int64_t t_frame_us, uint8_t* out) {
+  NvtxRange nvtx_range_("esi_render");
   return esi_render_many(h, &t_frame_us, 1, out);
 }
 
 int esi_get_state(esi_handle_t* h, float* S, int64_t* T) {
+  NvtxRange nvtx_range_("esi_get_state");
   if (!h) return ESI_ERR_INVALID_ARG;
   cudaSetDevice(h->prm.device);
   if (S) ESI_CUDA(h, cudaMemcpyAsync(S, h->dS, h->P * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
@@ -851,6 +871,7 @@ int esi_get_state(esi_handle_t* h, float* S, int64_t* T) {
 }
 
 int esi_set_state(esi_handle_t* h, const float* S, const int64_t* T) {
+  NvtxRange nvtx_range_("esi_set_state");
   if (!h || !S || !T) return ESI_ERR_INVALID_ARG;
   if (h->sticky) return h->sticky;
   cudaSetDevice(h->prm.device);
@@ -925,6 +946,7 @@ int esi_router_create(int32_t device, int32_t height, const int32_t* row_start, 
 }
 
 int esi_router_count(esi_router_t* r, const esi_event_t* events, size_t n, int64_t* counts, void* stream) {
+  NvtxRange nvtx_range_("esi_router_count");
   if (!r || !counts) return ESI_ERR_INVALID_ARG;
   r->counted = false;
   if (n == 0) {
@@ -972,6 +994,7 @@ int esi_router_count(esi_router_t* r, const esi_event_t* events, size_t n, int64
 }
 
 int esi_router_scatter(esi_router_t* r, esi_event_t* const* dst, const int64_t* dst_offset, void* stream) {
+  NvtxRange nvtx_range_("esi_router_scatter");
   if (!r || !dst || !dst_offset || !r->counted) return ESI_ERR_INVALID_ARG;
   if (r->n == 0) return ESI_OK;
   RouteDst d;
@@ -1003,6 +1026,7 @@ void esi_router_destroy(esi_router_t* r) {
 int esi_route_bands(int32_t device, const esi_event_t* events, size_t n, int32_t height,
                     const int32_t* row_start, int32_t n_bands, esi_event_t* out, int64_t* counts,
                     void* stream) {
+  NvtxRange nvtx_range_("esi_route_bands");
   if (!counts) return ESI_ERR_INVALID_ARG;
   if (int rc = router_check_rows(height, row_start, n_bands)) return rc;
   if (n == 0) {
@@ -1130,6 +1154,7 @@ int esi_stream_sync(int32_t device, void* stream) {
 }
 
 int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, esi_slice_map_t* maps) {
+  NvtxRange nvtx_range_("esi_slice_summarize");
   if (!h || !maps || (n && !events)) return ESI_ERR_INVALID_ARG;
   if (h->sticky) return h->sticky;
   cudaSetDevice(h->prm.device);
@@ -1221,6 +1246,7 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
 
 int esi_slice_compose(esi_handle_t* h, const esi_slice_map_t* first, const esi_slice_map_t* second,
                       esi_slice_map_t* out) {
+  NvtxRange nvtx_range_("esi_slice_compose");
   if (!h || !first || !second || !out) return ESI_ERR_INVALID_ARG;
   if (h->sticky) return h->sticky;
   cudaSetDevice(h->prm.device);
@@ -1229,6 +1255,7 @@ int esi_slice_compose(esi_handle_t* h, const esi_slice_map_t* first, const esi_s
 }
 
 int esi_slice_apply(esi_handle_t* h, const esi_slice_map_t* maps) {
+  NvtxRange nvtx_range_("esi_slice_apply");
   if (!h || !maps) return ESI_ERR_INVALID_ARG;
   if (h->sticky) return h->sticky;
   if (!h->segs.empty()) return ESI_ERR_INVALID_ARG;
