@@ -483,6 +483,55 @@ def run_c5b(args, ctx, peaks):
             "gpu_launches": None, "notes": {"generation_s": gen_s}}, w
 
 
+# --------------------------------------------------------------------------- c4t: time shards
+def run_c4t(args, ctx, peaks):
+    """the c4 stream sharded in time over the ranks
+    (dist.TimeSharded): every rank summarises its slice into per-pixel maps,
+    the maps are all-gathered (NCCL), rank r composes the maps of the earlier
+    slices, applies them to its initial state and integrates + renders its own
+    slice.  value = events of the whole stream / max-over-ranks step time."""
+    from esi_synth import make_workload
+    from paper_2508_02238_b200.dist import TimeSharded, time_slices
+    rank, world = ctx.rank, ctx.world
+    t0 = time.time()
+    w = make_workload("c4", "cuda", fps=args.fps)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    tf = np.asarray(w.t_frames)
+    t_ev = w.events[:, 0].cpu().numpy()
+    eb, fb = time_slices(t_ev, tf, world)
+    ev = w.events[eb[rank]:eb[rank + 1]]
+    tfr = tf[fb[rank]:fb[rank + 1]]
+    out = torch.empty((len(tfr), w.H, w.W), dtype=torch.uint8, device="cuda")
+    ts = TimeSharded(w.W, w.H, validate_on_push=1 if args.validation == "push" else 0, **w.params)
+
+    def step():
+        ts.run(ev, tfr, out)
+
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(ctx.local) as clk:
+        t_wall0 = time.time()
+        ms_total = ctx.timed(step, args.steps)
+        clk.mark(t_wall0, time.time())
+    # the scan's share: summarise + gather + compose + apply alone
+    n_sc = max(1, min(args.steps, 3))
+    ms_scan = ctx.timed(lambda: ts.incoming_state_maps(ev), n_sc) / n_sc
+    ts.close()
+    ms_step = ms_total / args.steps
+    cfg = {"workload": f"c4 time-sharded: {w.W}x{w.H}, {w.duration_us / 1e6:g} s stream, {w.n} events, "
+                       f"{len(tf)} frames @{args.fps} FPS, split in {world} time slices",
+           "sensor": f"{w.W}x{w.H}", "events_per_step": w.n, "events_per_step_per_gpu": eb[rank + 1] - eb[rank],
+           "frames_per_step": len(tf), "esi_params": w.params, "validation": args.validation,
+           "parallelism": f"time slices x{world} (per-pixel slice maps all-gathered + exclusive scan)"}
+    return {"value": w.n * args.steps / (ms_total / 1e3), "ms_per_step": ms_step,
+            "frames_per_s": len(tf) * args.steps / (ms_total / 1e3),
+            "stages": {"slice_map_scan_ms": ms_scan,
+                       "note": "esi_slice_summarize + all_gather + compose + apply (skipped at N=1)"},
+            "clocks": clk.summary(), "config": cfg, "e2e": None, "scaling": "strong", "gpu_launches": None,
+            "notes": {"generation_s": gen_s}}, w
+
+
 # --------------------------------------------------------------------------- streaming latency
 def run_latency(args, frames_max=300):
     """Analogue of the paper's per-frame reconstruction time (Fig. rec_time,
@@ -600,7 +649,7 @@ def parse_args(argv):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="esi", choices=["esi", "reference"])
-    ap.add_argument("--config", default="c4", choices=["c4", "c5a", "c5b"])
+    ap.add_argument("--config", default="c4", choices=["c4", "c5a", "c5b", "c4t"])
     ap.add_argument("--fps", type=int, default=100)
     ap.add_argument("--validation", default="push", choices=["push", "fused"],
                     help="push: validate_on_push=1 (the library default, atomic push); fused: checks in K1")
@@ -630,6 +679,8 @@ def main(argv=None):
         peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {}) or {}
         if args.config == "c5b":
             res, w = run_c5b(args, ctx, peaks)
+        elif args.config == "c4t":
+            res, w = run_c4t(args, ctx, peaks)
         else:
             res, w = run_streams(args, ctx, peaks)
         cpu = None

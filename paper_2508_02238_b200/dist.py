@@ -433,10 +433,14 @@ class TimeSharded:
         if handle_factory is None:
             from .esi import Esi as handle_factory
         self.group = group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
+        init = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if init else 0
+        self.world = dist.get_world_size(group) if init else 1
         self.h = handle_factory(width, height, **params)
-        self.timing = {}
+        if torch.cuda.is_available() and hasattr(self.h, "set_stream"):
+            # on torch's current stream: ordered after NCCL's all_gather of the maps
+            # and visible to CUDA events recorded on that stream
+            self.h.set_stream(torch.cuda.current_stream().cuda_stream)
 
     def close(self):
         if self.h is not None:
@@ -445,6 +449,8 @@ class TimeSharded:
 
     def incoming_state_maps(self, events_slice):
         """Steps 1-3: the exclusive prefix of the slices' maps (None on rank 0)."""
+        if self.world == 1:
+            return None
         maps = self.h.slice_summarize(events_slice)
         gathered = [torch.empty_like(maps) for _ in range(self.world)]
         dist.all_gather(gathered, maps, group=self.group)
