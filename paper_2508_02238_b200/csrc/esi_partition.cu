@@ -254,14 +254,15 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
       }
     }
   }
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // copy complete before the CTA retires
+  // the CTA may retire once the bulk copy has READ the sorted tile out of shared
+  // memory; the global writes complete asynchronously (K2 runs after this kernel)
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 template <int RANK, bool VALIDATE, bool BAND32>
 __global__ void __launch_bounds__(kPartThreads, kPartCtas) esi_partition_kernel(PartArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  // Chunk entirely after the last frame of this render: nothing to integrate.
-  if (a.ev[0].t_us > a.t_cap) return;
+  // (the host launches K1 only for chunks whose first event is <= the render's last frame)
   const int tile = blockIdx.x;
   const int ne = (int)min((int64_t)kTile, a.n - (int64_t)tile * kTile);
   if (ne == kTile) partition_tile<RANK, VALIDATE, BAND32, true>(a, smem, tile, ne);

@@ -757,10 +757,13 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.tile_wide = h->tile_wide[bf];
       pa.wide_t = h->wide_t[bf];
       pa.err = h->d_err;
-      TimedLaunch t1;
-      timed_begin(h, 0, &t1, k1s);
-      ESI_CUDA(h, launch_partition(pa, n_tiles, h->rank_mode, k1s));
-      timed_end(h, &t1);
+      if (hinfo[c].active) {   // a chunk entirely after the last frame (only chunk 0 can be) is not partitioned
+        TimedLaunch t1;
+        timed_begin(h, 0, &t1, k1s);
+        ESI_CUDA(h, launch_partition(pa, n_tiles, h->rank_mode, k1s));
+        timed_end(h, &t1);
+        h->st_launches += 1;
+      }
       if (two || any_host) ESI_CUDA(h, cudaEventRecord(h->ev_k1[bf], k1s));
       if (two) ESI_CUDA(h, cudaStreamWaitEvent(st, h->ev_k1[bf], 0));
 
@@ -802,7 +805,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
         const size_t nbytes = (size_t)(hinfo[c].f_hi - hinfo[c].f_lo) * (size_t)h->P;
         ESI_CUDA(h, cudaMemcpyAsync(out + o, dout + o, nbytes, cudaMemcpyDeviceToHost, h->d2h));
       }
-      h->st_launches += 2;
+      h->st_launches += 1;
       h->st_chunks += 1;
       index_base += ch.n;
     }
