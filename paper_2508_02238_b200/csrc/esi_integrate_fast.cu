@@ -247,8 +247,13 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
 }
 
 
+// register budget: as for ESI_K2_MINB CTAs per SM (default: the resident count the
+// bands are sized for); a larger value leaves registers for a co-resident K1 CTA
+#ifndef ESI_K2_MINB
+#define ESI_K2_MINB kK2Ctas
+#endif
 template <int BM>
-__global__ void __launch_bounds__(kNT, kK2Ctas) esi_integrate_kernel(IntArgs a) {
+__global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_wsum[32];
   const int band = blockIdx.x;

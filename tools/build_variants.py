@@ -6,6 +6,15 @@ VARIANTS = {
     "k2c2": ["-DESI_K2_CTAS=2"],
     "k2c2_t2048": ["-DESI_K2_CTAS=2", "-DESI_TILE=2048", "-DESI_PART_THREADS=256", "-DESI_PART_CTAS=2"],
     "t2048c3": ["-DESI_TILE=2048", "-DESI_PART_THREADS=256", "-DESI_PART_CTAS=3"],
+    # K1 with 8 warps per 4096-event tile: fewer registers per CTA, so that a K1 CTA
+    # fits beside two K2 CTAs on an SM (register file: 2 x 18.4 K + 20 K < 64 K)
+    "p256": ["-DESI_PART_THREADS=256", "-DESI_PART_CTAS=2"],
+    "p256c3": ["-DESI_PART_THREADS=256", "-DESI_PART_CTAS=3"],
+    # K2 at 2 CTAs per SM with a 3-CTA register budget + a light K1 (8 warps, 3072-event
+    # tiles, 6 Mi-event chunks) that fits beside them: K1 of chunk c+1 co-resident with K2 of c
+    "overlap": ["-DESI_K2_CTAS=2", "-DESI_K2_MINB=3", "-DESI_TILE=3072", "-DESI_PART_THREADS=256",
+                "-DESI_PART_CTAS=3"],
+    "overlap4k": ["-DESI_K2_CTAS=2", "-DESI_K2_MINB=3", "-DESI_PART_THREADS=256", "-DESI_PART_CTAS=3"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 os.makedirs(os.path.join(b.HERE, "variants"), exist_ok=True)
