@@ -201,7 +201,7 @@ cudaError_t launch_fill_i64(int64_t* p, int64_t n, int64_t v, cudaStream_t s);
 cudaError_t launch_frame_metrics(const uint8_t* frames, const float* truth, int64_t P, int n_frames,
                                  int truth_per_frame, double* pearson, double* mse_norm, cudaStream_t s);
 // time-sharded streams (esi_slice.cu)
-cudaError_t launch_slice_summary(const IntArgs& a, int64_t tbase, esi_slice_map_t* maps, cudaStream_t s);
+cudaError_t launch_slice_summary(const IntArgs& a, int64_t tbase, esi_slice_map_t* maps, int fast, cudaStream_t s);
 cudaError_t launch_slice_compose(const esi_slice_map_t* A, const esi_slice_map_t* B, esi_slice_map_t* out, int64_t P,
                                  const DecayParams& dp, const MapParams& mp, cudaStream_t s);
 cudaError_t launch_slice_apply(const esi_slice_map_t* M, float* S, int64_t* T, int64_t P, const DecayParams& dp,

@@ -1235,7 +1235,7 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     ia.dp = h->dp;
     ia.mp = h->mp;
     e = launch_partition(pa, n_tiles, h->rank_mode, st);
-    if (e == cudaSuccess) e = launch_slice_summary(ia, t01[0], maps, st);
+    if (e == cudaSuccess) e = launch_slice_summary(ia, t01[0], maps, h->allow_fast ? 1 : 0, st);
     if (e != cudaSuccess) fail(cuda_fail(h, e));
   }
   if (!rc) {

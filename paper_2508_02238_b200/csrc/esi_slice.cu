@@ -63,10 +63,11 @@ struct SliceStatic {
 };
 
 __host__ __device__ inline size_t r16s(size_t b) { return (b + 15) & ~(size_t)15; }
-// dynamic: G[bp] (float4), tl[bp] (int64), n[bp] (int32), h8[kSW][bp], off[bp + 1], pre[n_tiles + 1], mo[n_tiles]
-__host__ __device__ inline size_t sl_off_tl(int bp) { return (size_t)bp * 16; }
-__host__ __device__ inline size_t sl_off_n(int bp) { return sl_off_tl(bp) + (size_t)bp * 8; }
-__host__ __device__ inline size_t sl_off_h8(int bp) { return sl_off_n(bp) + (size_t)bp * 4; }
+// dynamic: h8[kSW][bp], off[bp + 1], pre[n_tiles + 1], mo[n_tiles]; the summaries
+// themselves stay in global memory (L2): a pixel's map is read and written once
+// per pass by the thread that folds its run, which keeps the CTA at 67 KB of shared
+// memory (3 CTAs per SM, one wave of bands)
+__host__ __device__ inline size_t sl_off_h8(int) { return 0; }
 __host__ __device__ inline size_t sl_off_off(int bp) { return sl_off_h8(bp) + (size_t)kSW * bp; }
 __host__ __device__ inline size_t sl_off_pre(int bp) { return sl_off_off(bp) + r16s((size_t)(bp + 1) * 2); }
 __host__ __device__ inline size_t sl_off_mo(int bp, int nt) { return sl_off_pre(bp) + r16s((size_t)(nt + 1) * 4); }
@@ -74,7 +75,19 @@ __host__ __device__ inline size_t sl_smem_bytes(int bp, int nt) { return sl_off_
 
 #include "esi_fast_common.cuh"
 
-__global__ void __launch_bounds__(kST, 1) esi_slice_summary_kernel(IntArgs a, int64_t tbase, esi_slice_map_t* maps) {
+// Decay of one event gap (Eq. 4): BM >= 0 -- the fast fp32 form of K2 (exact for
+// dt < 2^24 us after the cutoff clamp; handles with dt_cut < 2^23); BM < 0 -- the
+// general esi_decay (fp64 u for slow decays).
+template <int BM>
+__device__ __forceinline__ Map4 event_map_t(int64_t dt, int p, const IntArgs& a, const FastConst& kc) {
+  if (BM < 0) return event_map(dt, p, a.dp, a.mp);
+  const float d = ev_decay<(BM < 0 ? 0 : BM)>((float)min(dt, a.dp.dt_cut + 1), kc);
+  const float pc = p < 0 ? -kc.C : kc.C;
+  return Map4{d, (BM & kFirst) ? pc : d * pc, kc.smin, kc.smax};
+}
+
+template <int BM>
+__global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs a, int64_t tbase, esi_slice_map_t* maps) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(16) SliceStatic ss;
   const int band = blockIdx.x;
@@ -83,9 +96,6 @@ __global__ void __launch_bounds__(kST, 1) esi_slice_summary_kernel(IntArgs a, in
   const int64_t px0 = (int64_t)band * bp;
   const int npx = (int)min((int64_t)bp, a.P - px0);
   const int n_tiles = a.n_tiles;
-  float4* const G = reinterpret_cast<float4*>(smem_raw);
-  int64_t* const tl = reinterpret_cast<int64_t*>(smem_raw + sl_off_tl(bp));
-  int32_t* const cnt = reinterpret_cast<int32_t*>(smem_raw + sl_off_n(bp));
   uint8_t* const h8 = smem_raw + sl_off_h8(bp);
   uint16_t* const off = reinterpret_cast<uint16_t*>(smem_raw + sl_off_off(bp));
   uint32_t* const pre = reinterpret_cast<uint32_t*>(smem_raw + sl_off_pre(bp));
@@ -93,16 +103,7 @@ __global__ void __launch_bounds__(kST, 1) esi_slice_summary_kernel(IntArgs a, in
 
   // tbase: the chunk's first event; every event of the chunk is within 2^31 us of it (host check)
   const uint32_t tb32 = (uint32_t)tbase;
-  for (int i = tid; i < bp; i += kST) {
-    if (i < npx) {
-      const esi_slice_map_t m = maps[px0 + i];
-      G[i] = make_float4(m.a, m.c, m.lo, m.hi);
-      tl[i] = m.t_last;
-      cnt[i] = m.n;
-    } else {
-      cnt[i] = 0;
-    }
-  }
+  const FastConst kc = make_const(a);
   for (int i = tid; i < kSW * bp / 16; i += kST) reinterpret_cast<uint4*>(h8)[i] = make_uint4(0u, 0u, 0u, 0u);
   const int n_b = band_run_prefix<kSW>(a.meta + (int64_t)band * n_tiles, n_tiles, pre, mo, ss.misc + 32);
   __syncthreads();
@@ -205,43 +206,56 @@ __global__ void __launch_bounds__(kST, 1) esi_slice_summary_kernel(IntArgs a, in
     __syncthreads();
     for (int i = tid; i < kSW * bp / 16; i += kST) reinterpret_cast<uint4*>(h8)[i] = make_uint4(0u, 0u, 0u, 0u);
     // runs: thread t folds the runs that start in [8t, 8t + 8) into their pixels' summaries
-    for (int i = tid * kRunPT; i < min(n, tid * kRunPT + kRunPT); ++i) {
+    // (the next head's map is loaded while the current run is folded)
+    uint32_t heads = 0u;
+    const int r0 = tid * kRunPT;
+#pragma unroll
+    for (int u = 0; u < kRunPT; ++u) {
+      const int i = r0 + u;
+      if (i < n && (i == 0 || ((cur[i - 1].y ^ cur[i].y) & 0x7fffffffu) != 0u)) heads |= 1u << u;
+    }
+    esi_slice_map_t Mn;
+    int in_ = -1;
+    if (heads) {
+      in_ = r0 + __ffs(heads) - 1;
+      heads &= heads - 1u;
+      Mn = maps[px0 + (cur[in_].y & 0x7fffffffu)];
+    }
+    while (in_ >= 0) {
+      const int i = in_;
+      esi_slice_map_t M = Mn;
       const uint32_t px = cur[i].y & 0x7fffffffu;
-      if (i > 0 && (cur[i - 1].y & 0x7fffffffu) == px) continue;     // not the run's first event
+      in_ = -1;
+      if (heads) {                                       // prefetch the next run's map
+        in_ = r0 + __ffs(heads) - 1;
+        heads &= heads - 1u;
+        Mn = maps[px0 + (cur[in_].y & 0x7fffffffu)];
+      }
       const int o1 = off[px + 1];
-      float4 g4 = G[px];
-      Map4 g{g4.x, g4.y, g4.z, g4.w};
-      int64_t t_last = tl[px];
-      int32_t m = cnt[px];
+      Map4 g{M.a, M.c, M.lo, M.hi};
+      int64_t t_last = M.t_last;
+      int32_t m = M.n;
       for (int q = i; q < o1; ++q) {
         const uint2 r = cur[q];
         const int64_t t = tbase + (int64_t)(int32_t)(r.x - tb32);
         const int p = ((int32_t)r.y < 0) ? -1 : 1;
         if (m == 0) {                                    // the slice's first event at this pixel
-          esi_slice_map_t& o = maps[px0 + px];
-          o.t_first = t;
-          o.p_first = p;
+          M.t_first = t;
+          M.p_first = p;
           g = Map4{1.f, 0.f, -kBig, kBig};
         } else {
-          g = compose(event_map(t - t_last, p, a.dp, a.mp), g);
+          g = compose(event_map_t<BM>(t - t_last, p, a, kc), g);
         }
         t_last = t;
         ++m;
       }
-      G[px] = make_float4(g.a, g.c, g.lo, g.hi);
-      tl[px] = t_last;
-      cnt[px] = m;
+      M.a = g.a; M.c = g.c; M.lo = g.lo; M.hi = g.hi;
+      M.t_last = t_last;
+      M.n = m;
+      maps[px0 + px] = M;
     }
   }
   cp_async_wait_all();
-  __syncthreads();
-  for (int i = tid; i < npx; i += kST) {
-    esi_slice_map_t& o = maps[px0 + i];
-    const float4 g4 = G[i];
-    o.a = g4.x; o.c = g4.y; o.lo = g4.z; o.hi = g4.w;
-    o.t_last = tl[i];
-    o.n = cnt[i];
-  }
 }
 
 // out = A then B (A earlier), per pixel
@@ -279,19 +293,31 @@ __global__ void esi_slice_apply_kernel(const esi_slice_map_t* M, float* S, int64
 
 size_t slice_smem_bytes(int band_px, int n_tiles) { return sl_smem_bytes(band_px, n_tiles); }
 
-cudaError_t launch_slice_summary(const IntArgs& a, int64_t tbase, esi_slice_map_t* maps, cudaStream_t s) {
+template <int BM>
+cudaError_t launch_slice_summary_b(const IntArgs& a, int64_t tbase, esi_slice_map_t* maps, cudaStream_t s) {
   const size_t smem = sl_smem_bytes(a.band_px, a.n_tiles);
   int dev = 0;
   cudaGetDevice(&dev);
   static int configured[64] = {0};
   if (dev < 0 || dev >= 64 || !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(esi_slice_summary_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(esi_slice_summary_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sl_smem_bytes(kMaxBandPx, kMaxTilesPerChunk));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev] = 1;
   }
-  esi_slice_summary_kernel<<<a.nb, kST, smem, s>>>(a, tbase, maps);
+  esi_slice_summary_kernel<BM><<<a.nb, kST, smem, s>>>(a, tbase, maps);
   return cudaGetLastError();
+}
+
+cudaError_t launch_slice_summary(const IntArgs& a, int64_t tbase, esi_slice_map_t* maps, int fast, cudaStream_t s) {
+  if (!fast) return launch_slice_summary_b<-1>(a, tbase, maps, s);
+  if (a.dp.first)
+    return a.dp.bmode == 2           ? launch_slice_summary_b<2 + kFirst>(a, tbase, maps, s)
+           : a.dp.bmode == kDecayExp ? launch_slice_summary_b<kDecayExp + kFirst>(a, tbase, maps, s)
+                                     : launch_slice_summary_b<kFirst>(a, tbase, maps, s);
+  return a.dp.bmode == 2           ? launch_slice_summary_b<2>(a, tbase, maps, s)
+         : a.dp.bmode == kDecayExp ? launch_slice_summary_b<kDecayExp>(a, tbase, maps, s)
+                                   : launch_slice_summary_b<0>(a, tbase, maps, s);
 }
 
 cudaError_t launch_slice_compose(const esi_slice_map_t* A, const esi_slice_map_t* B, esi_slice_map_t* out, int64_t P,
