@@ -3,6 +3,7 @@
 //   esi_plan_kernel       : how many chunks start at or before the last frame
 //   esi_consume_kernel    : how many events of a segment were integrated
 //   esi_validate_kernel   : eager validation for params.validate_on_push
+#include <algorithm>
 #include "esi_device.cuh"
 
 namespace esi {
@@ -103,47 +104,70 @@ cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int
   return cudaGetLastError();
 }
 
-__device__ __forceinline__ void validate_one(int64_t i, int64_t n, int4 r, int64_t tp0, int lane, int64_t t_origin,
-                                             int64_t last_frame_t, int32_t W, int32_t H, unsigned long long* err) {
-  const bool in = i < n;
-  const int64_t t = (int64_t)(((uint64_t)(uint32_t)r.y << 32) | (uint32_t)r.x);
-  int64_t tp = __shfl_up_sync(0xffffffffu, t, 1);
-  if (lane == 0) tp = tp0;
-  const uint32_t x = (uint32_t)r.z & 0xffffu, y = (uint32_t)r.z >> 16;
-  const int p = (int)(int8_t)(r.w & 0xff);
-  if (in && ((x >= (uint32_t)W) | (y >= (uint32_t)H) | (p * p != 1) | (t < t_origin) | (t < tp) | (t <= last_frame_t))) {
-    int code;
-    if (x >= (uint32_t)W || y >= (uint32_t)H) code = ESI_ERR_OUT_OF_BOUNDS;
-    else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
-    else code = ESI_ERR_NEGATIVE_INTERVAL;
-    atomicMin(err, ((unsigned long long)i << 8) | (unsigned)code);
-  }
+// Eager validation of one push (reading A15), K0.  Each warp owns
+// a contiguous range of the batch and walks it in steps of 32 x kVU events:
+// lane l loads events step + l + 32 u (kVU coalesced 16-byte streaming loads in
+// flight per lane), the predecessor's t comes from the neighbouring lane by
+// shuffle and, for lane 0, from lane 31 of the previous row -- carried across
+// steps, so only a warp's first event needs a global load of its predecessor.
+constexpr int kVU = 8;
+
+__device__ __forceinline__ void report_bad(int64_t i, uint32_t x, uint32_t y, int p, int32_t W, int32_t H,
+                                           unsigned long long* err) {
+  int code;
+  if (x >= (uint32_t)W || y >= (uint32_t)H) code = ESI_ERR_OUT_OF_BOUNDS;
+  else if (p != 1 && p != -1) code = ESI_ERR_BAD_POLARITY;
+  else code = ESI_ERR_NEGATIVE_INTERVAL;
+  atomicMin(err, ((unsigned long long)i << 8) | (unsigned)code);
 }
 
-// Eager validation of one push (reading A15).  Four coalesced
-// 16-byte loads in flight per thread (streaming, read once); the predecessor's
-// t comes from the neighbouring lane, lane 0 loads it alongside its own events
-// (issued with them, so a warp waits for one memory latency per 128 events).
 __global__ void __launch_bounds__(256) esi_validate_kernel(const esi_event_t* ev, int64_t n, const int64_t* prev_t,
-                                                           int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
+                                                           int64_t t_min, int32_t W, int32_t H,
                                                            unsigned long long* err) {
-  constexpr int U = 4;
   const int4* evv = reinterpret_cast<const int4*>(ev);
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U; base < n; base += stride) {
-    int4 r[U];
-    int64_t tp0[U];
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr int64_t kStep = 32 * kVU;
+  const int64_t steps = (n + kStep - 1) / kStep;
+  const int64_t s0 = steps * wid / n_warps, s1 = steps * (wid + 1) / n_warps;   // this warp's steps
+  if (s0 >= s1) return;
+  int64_t carry = 0;                                     // t of the event before this warp's range
+  if (lane == 0) carry = s0 > 0 ? __ldg(&ev[s0 * kStep - 1].t_us) : *prev_t;
+  for (int64_t st = s0; st < s1; ++st) {
+    const int64_t base = st * kStep;
+    int4 r[kVU];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = base + u * blockDim.x + threadIdx.x;
+    for (int u = 0; u < kVU; ++u) {
+      const int64_t i = base + u * 32 + lane;
       r[u] = i < n ? ld_stream16(evv + i) : make_int4(0, 0, 0, 0);
-      tp0[u] = 0;
-      if (lane == 0 && i < n) tp0[u] = i > 0 ? __ldg(&ev[i - 1].t_us) : *prev_t;
     }
+    bool any_bad = false;
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      validate_one(base + u * blockDim.x + threadIdx.x, n, r[u], tp0[u], lane, t_origin, last_frame_t, W, H, err);
+    for (int u = 0; u < kVU; ++u) {
+      const int64_t i = base + u * 32 + lane;
+      const int64_t t = (int64_t)(((uint64_t)(uint32_t)r[u].y << 32) | (uint32_t)r[u].x);
+      int64_t tp = __shfl_up_sync(kFull, t, 1);
+      const int64_t last = __shfl_sync(kFull, t, 31);
+      if (lane == 0) tp = carry;
+      carry = last;                                      // lane 0's predecessor in the next row
+      const uint32_t x = (uint32_t)r[u].z & 0xffffu, y = (uint32_t)r[u].z >> 16;
+      const int p = (int)(int8_t)(r[u].w & 0xff);
+      const bool bad = (i < n) & ((x >= (uint32_t)W) | (y >= (uint32_t)H) | (p * p != 1) | (t < t_min) | (t < tp));
+      any_bad |= bad;
+    }
+    if (__any_sync(kFull, any_bad)) {                    // rare: find and report the offending events
+#pragma unroll
+      for (int u = 0; u < kVU; ++u) {
+        const int64_t i = base + u * 32 + lane;
+        const int64_t t = (int64_t)(((uint64_t)(uint32_t)r[u].y << 32) | (uint32_t)r[u].x);
+        const int64_t tp = i == 0 ? *prev_t : __ldg(&ev[i - 1].t_us);
+        const uint32_t x = (uint32_t)r[u].z & 0xffffu, y = (uint32_t)r[u].z >> 16;
+        const int p = (int)(int8_t)(r[u].w & 0xff);
+        if ((i < n) && ((x >= (uint32_t)W) | (y >= (uint32_t)H) | (p * p != 1) | (t < t_min) | (t < tp)))
+          report_bad(i, x, y, p, W, H, err);
+      }
+    }
   }
 }
 
@@ -151,9 +175,11 @@ cudaError_t launch_validate(const esi_event_t* ev, int64_t n, const int64_t* pre
                             int64_t t_origin, int64_t last_frame_t, int32_t W, int32_t H,
                             unsigned long long* err, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  int64_t blocks = (n + 1023) / 1024;
+  // events must be >= t_origin and > the last rendered frame time (A15)
+  const int64_t t_min = last_frame_t == INT64_MIN ? t_origin : std::max(t_origin, last_frame_t + 1);
+  int64_t blocks = (n + 2047) / 2048;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  esi_validate_kernel<<<(int)blocks, 256, 0, s>>>(ev, n, prev_t, t_origin, last_frame_t, W, H, err);
+  esi_validate_kernel<<<(int)blocks, 256, 0, s>>>(ev, n, prev_t, t_min, W, H, err);
   return cudaGetLastError();
 }
 
