@@ -502,6 +502,15 @@ def test_2560x1440_sensor_full_frames():
     _prefix_check(w, 500_000, 100)
 
 
+def test_c5a_stream_full_frames():
+    """One of config 5a's 64 independent 1280x720 streams (10 Mev/s, seed 5000),
+    first 1 s: every pixel of 100 frames and the final state against the oracle
+    (the stream-sharded config; each rank runs such streams)."""
+    w = make_workload("c5a", "cuda", seed=5000, duration_us=1_000_000)
+    frac, n = _prefix_check(w, 1_000_000, 100)
+    assert n > 8_000_000
+
+
 def test_c2_at_1000_fps():
     """1000 FPS readout (BASELINE config 4 renders at 100 and 1000 FPS): 10x more
     frame windows per chunk, mostly near-empty (the sparse-window path)."""
