@@ -1,17 +1,19 @@
 // esi_partition.cu -- K1: event ingest + validation + stable partition by band.
 //
-// One CTA per tile of kTile (8192) consecutive pending events.  Each lane loads
-// one 16-byte esi_event_t per step (a warp reads 512 contiguous bytes), checks
-// it (reading A15: t non-decreasing, >= t_origin, > last frame),
-// and computes its pixel id y*W + x and its band = pid / band_px.  The tile
-// is then stably partitioned by band -- band-major, arrival-order-minor, i.e.
-// exactly std::stable_sort by band -- with
-//   * warp multi-split ranks from ballots over the band bits (no atomics, so
-//     the order is deterministic by construction),
-//   * per-warp band histograms in shared memory, a per-band prefix over warps
-//     and a block scan over bands,
-//   * a scatter into a shared-memory copy of the tile and one coalesced
-//     16-byte-vector write of the sorted tile.
+// One 512-thread CTA per tile of kTile (4096) consecutive pending events.  The
+// tile's 16-byte esi_event_t records are staged in shared memory with cp.async
+// (a warp reads 512 contiguous bytes per step, every load in flight at once);
+// each event is checked (reading A15: t non-decreasing, >=
+// t_origin, > last frame) unless the push validated it, and its pixel id
+// y*W + x and band = pid / band_px are computed.  The tile is then stably
+// partitioned by band -- band-major, arrival-order-minor, i.e. exactly
+// std::stable_sort by band -- with
+//   * per-warp band histograms in shared memory whose ranks come from one of
+//     three rank modes (lane-ordered shared atomics, probed at esi_create;
+//     peer masks; ballot multi-split -- the last two ordered by construction),
+//   * a per-band prefix over the warps (four bands per thread, packed u16
+//     pairs) and a warp-shuffle scan over the bands,
+//   * a scatter into shared memory and one TMA bulk copy of the sorted tile.
 // Record (8 B): x = low 32 bits of t, y = pixel-in-band | (p < 0) << 31.
 // meta[band][tile] = offset-in-tile | count << 16 tells K2 where its events are.
 #include "esi_device.cuh"
@@ -21,45 +23,8 @@ namespace esi {
 size_t partition_smem_bytes(int nb, int rank_mode) {
   const int nbp = (nb + 7) & ~7;
   return (size_t)kTile * sizeof(int4) + (size_t)kPartWarps * nbp * sizeof(uint16_t) +
-         (size_t)(nb + 1) * sizeof(uint32_t) + 64 * sizeof(uint32_t) +
+         (size_t)(nbp + 8) * sizeof(uint32_t) + 64 * sizeof(uint32_t) +
          (rank_mode == 2 ? (size_t)kPartWarps * nbp * sizeof(uint32_t) : 0);
-}
-
-// Exclusive scan of v[0..n) in place (n <= 4 * kPartThreads); v[n] = total.
-__device__ void part_block_exclusive_scan(uint32_t* v, int n, uint32_t* wsum) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int i0 = 4 * tid;
-  uint32_t a[4], s = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    a[q] = i0 + q < n ? v[i0 + q] : 0u;
-    s += a[q];
-  }
-  uint32_t x = s;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = lane < kPartWarps ? wsum[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, w, o);
-      if (lane >= o) w += y;
-    }
-    wsum[32 + lane] = w;  // inclusive warp totals
-  }
-  __syncthreads();
-  uint32_t run = x - s + (warp ? wsum[32 + warp - 1] : 0u);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (i0 + q < n) v[i0 + q] = run;
-    run += a[q];
-  }
-  if (tid == 0) v[n] = wsum[32 + kPartWarps - 1];
 }
 
 // RANK_ATOMIC: per-warp rank from a shared-memory atomicAdd on the warp's private
@@ -79,8 +44,8 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   int4* raw = reinterpret_cast<int4*>(smem);                     // [kTile] staged records
   uint2* sbuf = reinterpret_cast<uint2*>(smem);                  // [kTile] sorted records (aliases raw)
   uint16_t* hist = reinterpret_cast<uint16_t*>(raw + kTile);     // [kPartWarps][nbp]
-  uint32_t* boff = reinterpret_cast<uint32_t*>(hist + kPartWarps * nbp);  // [nb + 1]
-  uint32_t* wsum = boff + a.nb + 1;                               // [64]
+  uint32_t* boff = reinterpret_cast<uint32_t*>(hist + kPartWarps * nbp);  // [nbp + 8]
+  uint32_t* wsum = boff + nbp + 8;                                // [64]
   uint32_t* pmask = wsum + 64;                                    // RANK 2: [kPartWarps][nbp] peer masks (zero)
   __shared__ int s_wide;
   __shared__ int64_t s_tprev;
@@ -111,6 +76,12 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   if (threadIdx.x == 0) s_tprev = tile > 0 ? ev[-1].t_us : *a.prev_t;   // predecessor of the tile's first event
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 0) {                        // tile time base (from the staged records)
+    const int64_t t0 = *reinterpret_cast<const int64_t*>(raw), t1 = *reinterpret_cast<const int64_t*>(raw + ne - 1);
+    a.tile_t0[tile] = t0;
+    s_wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
+    a.tile_wide[tile] = s_wide;
+  }
 
   uint16_t* myhist = hist + warp * nbp;
   uint32_t key[EPT], tl[EPT], pr[EPT];   // band | rank << 10; record words (t low, pixel | sign)
@@ -194,25 +165,52 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   }
   __syncthreads();                               // raw consumed: its first half becomes sbuf
 
-  // per band: exclusive prefix over the warps, band total into boff[band]
-  for (int b = threadIdx.x; b < a.nb; b += kPartThreads) {
-    uint32_t run = 0;
+  // Per band: exclusive prefix over the warps' counts, then an exclusive scan over
+  // the bands -> boff, and the band's meta entry.  Four bands per thread as two
+  // packed u16 pairs (a warp counts <= 256 events of a band, a tile <= 4096, so
+  // the halves never carry); the threads with bands are whole warps at the front.
+  const int nq4 = nbp >> 2;                      // nbp is a multiple of 8
+  const int b0 = 4 * (int)threadIdx.x;
+  uint32_t t01 = 0, t23 = 0, loc = 0, incl = 0;
+  if ((int)threadIdx.x < nq4) {
+    uint32_t lo = 0, hi = 0;
 #pragma unroll
     for (int w = 0; w < kPartWarps; ++w) {
-      const uint32_t c = hist[w * nbp + b];
-      hist[w * nbp + b] = (uint16_t)run;
-      run += c;
+      uint2* hp = reinterpret_cast<uint2*>(hist + w * nbp + b0);
+      const uint2 c = *hp;
+      *hp = make_uint2(lo, hi);
+      lo += c.x;
+      hi += c.y;
     }
-    boff[b] = run;
+    t01 = lo;
+    t23 = hi;
+    loc = (lo & 0xffffu) + (lo >> 16) + (hi & 0xffffu) + (hi >> 16);
+  }
+  const int nqw = (nq4 + 31) >> 5;               // warps holding bands
+  if (warp < nqw) {
+    incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
   }
   __syncthreads();
-  part_block_exclusive_scan(boff, a.nb, wsum);
+  if ((int)threadIdx.x < nq4) {
+    uint32_t o0 = incl - loc;
+    for (int w = 0; w < warp; ++w) o0 += wsum[w];
+    const uint32_t c0 = t01 & 0xffffu, c1 = t01 >> 16, c2 = t23 & 0xffffu, c3 = t23 >> 16;
+    const uint32_t o1 = o0 + c0, o2 = o1 + c1, o3 = o2 + c2;
+    *reinterpret_cast<uint4*>(boff + b0) = make_uint4(o0, o1, o2, o3);
+    uint32_t* mp = a.meta + (int64_t)b0 * gridDim.x + tile;
+    if (b0 < a.nb) mp[0] = o0 | (c0 << 16);
+    if (b0 + 1 < a.nb) mp[gridDim.x] = o1 | (c1 << 16);
+    if (b0 + 2 < a.nb) mp[2 * gridDim.x] = o2 | (c2 << 16);
+    if (b0 + 3 < a.nb) mp[3 * gridDim.x] = o3 | (c3 << 16);
+  }
   __syncthreads();
 
-  for (int b = threadIdx.x; b < a.nb; b += kPartThreads) {
-    const uint32_t cnt = boff[b + 1] - boff[b];
-    a.meta[(int64_t)b * gridDim.x + tile] = boff[b] | (cnt << 16);
-  }
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     if (FULL || warp * WEV + r * 32 + lane < ne) {
@@ -221,12 +219,6 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
       ESI_DCHECK(band < (uint32_t)a.nb && pos < (uint32_t)ne);
       sbuf[pos] = make_uint2(tl[r], pr[r]);
     }
-  }
-  if (threadIdx.x == 0) {
-    const int64_t t0 = ev[0].t_us, t1 = ev[ne - 1].t_us;
-    a.tile_t0[tile] = t0;
-    s_wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
-    a.tile_wide[tile] = s_wide;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
