@@ -55,27 +55,36 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
   const esi_event_t* ev = a.ev + e0;
   const int4* evv = reinterpret_cast<const int4*>(ev);
 
-  // the raw events are read once: evict-first in L2, so that they do not push
-  // out the previous chunk's records that K2 is reading meanwhile
-  uint64_t pol_first;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-#pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int i = warp * WEV + r * 32 + lane;
-    if (FULL || i < ne) {
-      const uint32_t d = (uint32_t)__cvta_generic_to_shared(raw + i);
-      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(evv + i),
-                   "l"(pol_first) : "memory");
-    }
+  // The tile's raw records: one TMA bulk copy (16-byte multiple, 16-byte aligned)
+  // completed on an mbarrier, issued by thread 0 while the others clear the
+  // histograms.  The raw events are read once: evict-first in L2, so that they
+  // do not push out the previous chunk's records that K2 is reading meanwhile.
+  __shared__ __align__(8) uint64_t s_mbar;
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  if (threadIdx.x == 0) {
+    uint64_t pol_first;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t bytes = (uint32_t)ne * 16u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"((uint32_t)__cvta_generic_to_shared(raw)), "l"(evv), "r"(bytes), "r"(mbar), "l"(pol_first)
+                 : "memory");
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int i = threadIdx.x; i < kPartWarps * nbp / 8; i += kPartThreads)
     reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
   if (RANK == 2)
     for (int i = threadIdx.x; i < kPartWarps * nbp; i += kPartThreads) pmask[i] = 0u;
-  if (threadIdx.x == 0) s_tprev = tile > 0 ? ev[-1].t_us : *a.prev_t;   // predecessor of the tile's first event
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
+  if (VALIDATE && threadIdx.x == 0) s_tprev = tile > 0 ? ev[-1].t_us : *a.prev_t;   // predecessor of the tile's first event
+  __syncthreads();                               // mbarrier initialised, histograms clear
+  {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+                   : "=r"(done) : "r"(mbar) : "memory");
+  }
   if (threadIdx.x == 0) {                        // tile time base (from the staged records)
     const int64_t t0 = *reinterpret_cast<const int64_t*>(raw), t1 = *reinterpret_cast<const int64_t*>(raw + ne - 1);
     a.tile_t0[tile] = t0;
