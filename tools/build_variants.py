@@ -3,6 +3,9 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_02238_b200 import build as b
 VARIANTS = {
+    "k2c4": ["-DESI_K2_CTAS=4"],
+    "k2c2w12": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=12"],
+    "k2c2w16": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=16"],
     "k2c2": ["-DESI_K2_CTAS=2"],
     "k2c2_t2048": ["-DESI_K2_CTAS=2", "-DESI_TILE=2048", "-DESI_PART_THREADS=256", "-DESI_PART_CTAS=2"],
     "t2048c3": ["-DESI_TILE=2048", "-DESI_PART_THREADS=256", "-DESI_PART_CTAS=3"],
