@@ -97,6 +97,8 @@ struct WideParams {
 struct PartArgs {
   const esi_event_t* ev;     // this chunk's events
   int64_t n;                 // events in the chunk
+  int32_t n_tiles;           // tiles of kTile events (set by launch_partition)
+  uint32_t* tile_ctr;        // [2] zero at launch: tiles claimed by the persistent CTAs, CTAs done
   int64_t index_base;        // index of ev[0] among this render's pending events
   const int64_t* prev_t;     // t of the event preceding ev[0] (device address)
   int64_t t_origin;

@@ -16,13 +16,14 @@
 //   * a scatter into shared memory and one TMA bulk copy of the sorted tile.
 // Record (8 B): x = low 32 bits of t, y = pixel-in-band | (p < 0) << 31.
 // meta[band][tile] = offset-in-tile | count << 16 tells K2 where its events are.
+#include <algorithm>
 #include "esi_device.cuh"
 
 namespace esi {
 
 size_t partition_smem_bytes(int nb, int rank_mode) {
   const int nbp = (nb + 7) & ~7;
-  return (size_t)kTile * sizeof(int4) + (size_t)kPartWarps * nbp * sizeof(uint16_t) +
+  return (size_t)kTile * sizeof(int4) + (size_t)kTile * sizeof(uint2) + (size_t)kPartWarps * nbp * sizeof(uint16_t) +
          (size_t)(nbp + 8) * sizeof(uint32_t) + 64 * sizeof(uint32_t) +
          (rank_mode == 2 ? (size_t)kPartWarps * nbp * sizeof(uint32_t) : 0);
 }
@@ -30,73 +31,64 @@ size_t partition_smem_bytes(int nb, int rank_mode) {
 // RANK_ATOMIC: per-warp rank from a shared-memory atomicAdd on the warp's private
 // (u16-packed) histogram -- relies on same-address lanes being served in lane
 // order, which esi_probe_atomic_order checks at esi_create; otherwise ranks come
-// from a ballot multi-split over the band bits (order by construction).
+// from peer masks or a ballot multi-split over the band bits (order by construction).
 // FULL: the tile holds kTile events (no bounds checks on the common path).
 //
-// The tile's raw 16-B records are staged in shared memory with cp.async (every
-// load of the tile in flight at once); the sorted tile later reuses the first
-// half of that buffer, after the records have been consumed into registers.
+// Persistent CTAs (grid = resident CTAs, tiles strided by gridDim.x).  A tile's
+// raw 16-B records are staged in shared memory by one TMA bulk copy completed on
+// an mbarrier; as soon as they are consumed into registers, thread 0 issues the
+// copy of the CTA's next tile, which lands while the current one is ranked,
+// scanned, scattered and written.  The sorted tile has its own buffer (sbuf),
+// written to global memory by one TMA bulk store.
+struct PartSmem {
+  int4* raw;          // [kTile] staged records
+  uint2* sbuf;        // [kTile] sorted records
+  uint16_t* hist;     // [kPartWarps][nbp]
+  uint32_t* boff;     // [nbp + 8]
+  uint32_t* wsum;     // [64]
+  uint32_t* pmask;    // RANK 2: [kPartWarps][nbp] peer masks (zero)
+};
+
+__device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(mbar), "r"(parity) : "memory");
+}
+
+// raw <- tile's records (thread 0 only)
+__device__ __forceinline__ void issue_tile_load(const PartArgs& a, const PartSmem& sm, int tile, uint32_t mbar) {
+  const int ne = (int)min((int64_t)kTile, a.n - (int64_t)tile * kTile);
+  uint64_t pol_first;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic reads of raw
+  const uint32_t bytes = (uint32_t)ne * 16u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"((uint32_t)__cvta_generic_to_shared(sm.raw)), "l"(a.ev + (int64_t)tile * kTile), "r"(bytes),
+               "r"(mbar), "l"(pol_first) : "memory");
+}
+
 template <int RANK, bool VALIDATE, bool BAND32, bool FULL>
-__device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char* smem, int tile, int ne) {
+__device__ __forceinline__ void partition_tile(const PartArgs& a, const PartSmem& sm, int tile, int ne,
+                                               uint32_t mbar, int64_t* s_tprev, int* s_wide, int* s_next) {
   constexpr int EPT = kTile / kPartThreads;                      // events per thread (8)
   constexpr int WEV = EPT * 32;                                  // events per warp (256)
   const int nbp = (a.nb + 7) & ~7;
-  int4* raw = reinterpret_cast<int4*>(smem);                     // [kTile] staged records
-  uint2* sbuf = reinterpret_cast<uint2*>(smem);                  // [kTile] sorted records (aliases raw)
-  uint16_t* hist = reinterpret_cast<uint16_t*>(raw + kTile);     // [kPartWarps][nbp]
-  uint32_t* boff = reinterpret_cast<uint32_t*>(hist + kPartWarps * nbp);  // [nbp + 8]
-  uint32_t* wsum = boff + nbp + 8;                                // [64]
-  uint32_t* pmask = wsum + 64;                                    // RANK 2: [kPartWarps][nbp] peer masks (zero)
-  __shared__ int s_wide;
-  __shared__ int64_t s_tprev;
-
+  int4* raw = sm.raw;
+  uint2* sbuf = sm.sbuf;
+  uint16_t* hist = sm.hist;
+  uint32_t* boff = sm.boff;
+  uint32_t* wsum = sm.wsum;
   const int64_t e0 = (int64_t)tile * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const esi_event_t* ev = a.ev + e0;
-  const int4* evv = reinterpret_cast<const int4*>(ev);
-
-  // The tile's raw records: one TMA bulk copy (16-byte multiple, 16-byte aligned)
-  // completed on an mbarrier, issued by thread 0 while the others clear the
-  // histograms.  The raw events are read once: evict-first in L2, so that they
-  // do not push out the previous chunk's records that K2 is reading meanwhile.
-  __shared__ __align__(8) uint64_t s_mbar;
-  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
-  if (threadIdx.x == 0) {
-    uint64_t pol_first;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const uint32_t bytes = (uint32_t)ne * 16u;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                 ::"r"((uint32_t)__cvta_generic_to_shared(raw)), "l"(evv), "r"(bytes), "r"(mbar), "l"(pol_first)
-                 : "memory");
-  }
-  for (int i = threadIdx.x; i < kPartWarps * nbp / 8; i += kPartThreads)
-    reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
-  if (RANK == 2)
-    for (int i = threadIdx.x; i < kPartWarps * nbp; i += kPartThreads) pmask[i] = 0u;
-  if (VALIDATE && threadIdx.x == 0) s_tprev = tile > 0 ? ev[-1].t_us : *a.prev_t;   // predecessor of the tile's first event
-  __syncthreads();                               // mbarrier initialised, histograms clear
-  {
-    uint32_t done = 0;
-    while (!done)
-      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
-                   : "=r"(done) : "r"(mbar) : "memory");
-  }
-  if (threadIdx.x == 0) {                        // tile time base (from the staged records)
-    const int64_t t0 = *reinterpret_cast<const int64_t*>(raw), t1 = *reinterpret_cast<const int64_t*>(raw + ne - 1);
-    a.tile_t0[tile] = t0;
-    s_wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
-    a.tile_wide[tile] = s_wide;
-  }
 
   uint16_t* myhist = hist + warp * nbp;
   uint32_t key[EPT], tl[EPT], pr[EPT];   // band | rank << 10; record words (t low, pixel | sign)
   const uint32_t W = (uint32_t)a.W, H = (uint32_t)a.H, BPX = (uint32_t)a.band_px;
   const int64_t t_min = a.t_min;
-  const int64_t tprev0 = s_tprev;
+  const int64_t tprev0 = VALIDATE ? *s_tprev : 0;
 
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
@@ -135,7 +127,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     } else if (RANK == 2) {
       // peers = the lanes of this round with my band: OR of lane bits into the warp's
       // mask of the band (order-independent), so ranks are lane (= arrival) order by construction
-      uint32_t* pm = pmask + warp * nbp;
+      uint32_t* pm = sm.pmask + warp * nbp;
       if (act) atomicOr(pm + band, 1u << lane);
       __syncwarp();
       const uint32_t peers = act ? pm[band] : 0u;
@@ -172,7 +164,21 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     pr[r] = pix | ((p < 0 && !(act && bad)) ? 0x80000000u : 0u);
     key[r] = band | (rank << 10);
   }
-  __syncthreads();                               // raw consumed: its first half becomes sbuf
+  __syncthreads();                               // raw consumed
+
+  if (threadIdx.x == 0) {                        // tile time base; then the next tile's records
+    const int64_t t0 = *reinterpret_cast<const int64_t*>(raw), t1 = *reinterpret_cast<const int64_t*>(raw + ne - 1);
+    a.tile_t0[tile] = t0;
+    *s_wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
+    a.tile_wide[tile] = *s_wide;
+    const int next = (int)atomicAdd(a.tile_ctr, 1u);   // the CTA's next tile (claimed in order)
+    *s_next = next;
+    if (next < a.n_tiles) {
+      if (VALIDATE) *s_tprev = a.ev[(int64_t)next * kTile - 1].t_us;   // the next tile's predecessor
+      issue_tile_load(a, sm, next, mbar);
+    }
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the previous sorted tile has left sbuf
+  }
 
   // Per band: exclusive prefix over the warps' counts, then an exclusive scan over
   // the bands -> boff, and the band's meta entry.  Four bands per thread as two
@@ -212,11 +218,12 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     const uint32_t c0 = t01 & 0xffffu, c1 = t01 >> 16, c2 = t23 & 0xffffu, c3 = t23 >> 16;
     const uint32_t o1 = o0 + c0, o2 = o1 + c1, o3 = o2 + c2;
     *reinterpret_cast<uint4*>(boff + b0) = make_uint4(o0, o1, o2, o3);
-    uint32_t* mp = a.meta + (int64_t)b0 * gridDim.x + tile;
+    const int nt = a.n_tiles;
+    uint32_t* mp = a.meta + (int64_t)b0 * nt + tile;
     if (b0 < a.nb) mp[0] = o0 | (c0 << 16);
-    if (b0 + 1 < a.nb) mp[gridDim.x] = o1 | (c1 << 16);
-    if (b0 + 2 < a.nb) mp[2 * gridDim.x] = o2 | (c2 << 16);
-    if (b0 + 3 < a.nb) mp[3 * gridDim.x] = o3 | (c3 << 16);
+    if (b0 + 1 < a.nb) mp[nt] = o1 | (c1 << 16);
+    if (b0 + 2 < a.nb) mp[2 * nt] = o2 | (c2 << 16);
+    if (b0 + 3 < a.nb) mp[3 * nt] = o3 | (c3 << 16);
   }
   __syncthreads();
 
@@ -244,7 +251,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
     if (ne & 1) a.rec[e0 + ne - 1] = sbuf[ne - 1];
   }
 
-  if (s_wide) {  // rare: tile spans >= 2^32 us; keep the full timestamps beside the records
+  if (*s_wide) {  // rare: tile spans >= 2^32 us; keep the full timestamps beside the records
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
       const int i = warp * WEV + r * 32 + lane;
@@ -254,20 +261,62 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, unsigned char*
         a.wide_t[e0 + pos] = ev[i].t_us;
       }
     }
+    __syncthreads();                             // hist is cleared next
   }
-  // the CTA may retire once the bulk copy has READ the sorted tile out of shared
-  // memory; the global writes complete asynchronously (K2 runs after this kernel)
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  // clear the histograms for the next tile (the loop's barrier orders it before the ranking)
+  for (int i = threadIdx.x; i < kPartWarps * nbp / 8; i += kPartThreads)
+    reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 template <int RANK, bool VALIDATE, bool BAND32>
 __global__ void __launch_bounds__(kPartThreads, kPartCtas) esi_partition_kernel(PartArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_mbar;
+  __shared__ int64_t s_tprev;
+  __shared__ int s_wide;
   // (the host launches K1 only for chunks whose first event is <= the render's last frame)
-  const int tile = blockIdx.x;
-  const int ne = (int)min((int64_t)kTile, a.n - (int64_t)tile * kTile);
-  if (ne == kTile) partition_tile<RANK, VALIDATE, BAND32, true>(a, smem, tile, ne);
-  else partition_tile<RANK, VALIDATE, BAND32, false>(a, smem, tile, ne);
+  const int nbp = (a.nb + 7) & ~7;
+  PartSmem sm;
+  sm.raw = reinterpret_cast<int4*>(smem);
+  sm.sbuf = reinterpret_cast<uint2*>(sm.raw + kTile);
+  sm.hist = reinterpret_cast<uint16_t*>(sm.sbuf + kTile);
+  sm.boff = reinterpret_cast<uint32_t*>(sm.hist + kPartWarps * nbp);
+  sm.wsum = sm.boff + nbp + 8;
+  sm.pmask = sm.wsum + 64;
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  __shared__ int s_next;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int t0 = (int)atomicAdd(a.tile_ctr, 1u);   // tiles are claimed dynamically: CTAs that start
+    s_next = t0;                                     // early (beside K2's tail) take more of them
+    if (t0 < a.n_tiles) {
+      if (VALIDATE) s_tprev = t0 > 0 ? a.ev[(int64_t)t0 * kTile - 1].t_us : *a.prev_t;
+      issue_tile_load(a, sm, t0, mbar);
+    }
+  }
+  for (int i = threadIdx.x; i < kPartWarps * nbp / 8; i += kPartThreads)
+    reinterpret_cast<uint4*>(sm.hist)[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (RANK == 2)
+    for (int i = threadIdx.x; i < kPartWarps * nbp; i += kPartThreads) sm.pmask[i] = 0u;
+  for (uint32_t k = 0;; ++k) {
+    __syncthreads();                             // histograms clear, s_next / s_tprev / s_wide settled
+    const int tile = s_next;
+    if (tile >= a.n_tiles) break;
+    mbar_wait_parity(mbar, k & 1u);              // this tile's records have landed
+    const int ne = (int)min((int64_t)kTile, a.n - (int64_t)tile * kTile);
+    if (ne == kTile) partition_tile<RANK, VALIDATE, BAND32, true>(a, sm, tile, ne, mbar, &s_tprev, &s_wide, &s_next);
+    else partition_tile<RANK, VALIDATE, BAND32, false>(a, sm, tile, ne, mbar, &s_tprev, &s_wide, &s_next);
+  }
+  if (threadIdx.x == 0) {                        // the last CTA out resets the counters for the next launch
+    if (atomicAdd(a.tile_ctr + 1, 1u) == gridDim.x - 1) {
+      a.tile_ctr[0] = 0u;
+      a.tile_ctr[1] = 0u;
+    }
+  }
+  // the CTA may retire once the last bulk store has READ sbuf; the global writes
+  // complete asynchronously (K2 runs after this kernel)
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 template <int RA, bool V, bool B32>
@@ -276,13 +325,27 @@ static cudaError_t launch_part_t(const PartArgs& a, int n_tiles, cudaStream_t s)
   int dev = 0;
   cudaGetDevice(&dev);
   static int configured[64] = {0};   // per device (the attribute is per context); the maximum once
-  if (dev < 0 || dev >= 64 || !configured[dev]) {
+  static int n_sm[64] = {0};
+  static int occ[64][2] = {{0}};      // resident CTAs per SM for band count occ[.][1]
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel<RA, V, B32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)partition_smem_bytes(kMaxBands, RA));
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) configured[dev] = 1;
+    configured[dev] = 1;
   }
-  esi_partition_kernel<RA, V, B32><<<n_tiles, kPartThreads, smem, s>>>(a);
+  if (occ[dev][1] != a.nb || occ[dev][0] <= 0) {
+    int o = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, esi_partition_kernel<RA, V, B32>, kPartThreads, smem);
+    if (e != cudaSuccess) return e;
+    occ[dev][0] = o > 0 ? o : 1;
+    occ[dev][1] = a.nb;
+  }
+  const int grid = (int)std::min<int64_t>(n_tiles, (int64_t)occ[dev][0] * n_sm[dev]);   // persistent CTAs
+  PartArgs b = a;
+  b.n_tiles = n_tiles;
+  esi_partition_kernel<RA, V, B32><<<grid, kPartThreads, smem, s>>>(b);
   return cudaGetLastError();
 }
 

@@ -78,6 +78,7 @@ struct esi_handle {
   uint32_t* meta[2] = {nullptr, nullptr};
   int64_t* tile_t0[2] = {nullptr, nullptr};
   int32_t* tile_wide[2] = {nullptr, nullptr};
+  uint32_t* tile_ctr = nullptr;   // [2][2] K1 work counters per scratch buffer: tiles claimed, CTAs done
   int64_t* wide_t[2] = {nullptr, nullptr};
   cudaStream_t aux = nullptr;               // K1 stream
   cudaStream_t h2d = nullptr, d2h = nullptr; // copy streams of the pinned-host pipeline
@@ -432,6 +433,8 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
               cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) != cudaSuccess))
     rc = ESI_ERR_CUDA;
   dalloc((void**)&h->d_err, sizeof(unsigned long long));
+  dalloc((void**)&h->tile_ctr, 4 * sizeof(uint32_t));
+  if (!rc && cudaMemset(h->tile_ctr, 0, 4 * sizeof(uint32_t)) != cudaSuccess) rc = ESI_ERR_CUDA;
   dalloc((void**)&h->d_last_t, sizeof(int64_t));
   dalloc((void**)&h->d_n_active, sizeof(int32_t));
   if (!rc) rc = ensure_pinned(h, 1 << 16);
@@ -483,7 +486,7 @@ void esi_destroy(esi_handle_t* h) {
   if (h->aux) cudaStreamSynchronize(h->aux);
   void* bufs[] = {h->dS, h->dT, h->rec[0], h->meta[0], h->tile_t0[0], h->tile_wide[0], h->wide_t[0],
                   h->rec[1], h->meta[1], h->tile_t0[1], h->tile_wide[1], h->wide_t[1], h->d_tf,
-                  (void*)h->d_chunk_first, h->d_chunk_n, h->d_info, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames,
+                  (void*)h->d_chunk_first, h->d_chunk_n, h->d_info, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames, h->tile_ctr,
                   h->dS_snap, h->dT_snap};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -698,6 +701,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     plan_range.reset();
     const int n_act = std::max(1, *hna);
     ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
+    ESI_CUDA(h, cudaMemsetAsync(h->tile_ctr, 0, 4 * sizeof(uint32_t), st));   // K1 work counters (robust to an aborted launch)
     const bool lazy = !h->prm.validate_on_push;
     if (lazy) {   // lazy validation (fused in K1): keep the state so that a failing render leaves it untouched
       if (!h->dS_snap) {
@@ -752,6 +756,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.band32 = h->band32 ? 1 : 0;
       pa.validate = h->prm.validate_on_push ? 0 : 1;
       pa.rec = h->rec[bf];
+      pa.tile_ctr = h->tile_ctr + 2 * bf;
       pa.meta = h->meta[bf];
       pa.tile_t0 = h->tile_t0[bf];
       pa.tile_wide = h->tile_wide[bf];
@@ -1220,6 +1225,7 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     pa.band32 = h->band32 ? 1 : 0;
     pa.validate = 0;   // validated above
     pa.rec = h->rec[0];
+    pa.tile_ctr = h->tile_ctr;
     pa.meta = h->meta[0];
     pa.tile_t0 = h->tile_t0[0];
     pa.tile_wide = h->tile_wide[0];
@@ -1300,6 +1306,7 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   pa.band32 = h->band32 ? 1 : 0;
   pa.validate = h->prm.validate_on_push ? 0 : 1;
   pa.rec = h->rec[0];
+  pa.tile_ctr = h->tile_ctr;
   pa.meta = h->meta[0];
   pa.tile_t0 = h->tile_t0[0];
   pa.tile_wide = h->tile_wide[0];
