@@ -128,24 +128,34 @@ __device__ __forceinline__ void apply_event(float* S, float* T, int px, uint2 ev
 // clamped affine maps s -> clamp(a s + c, lo, hi), a >= 0:
 // event i is f_i = (d_i, d_i p_i C, S_min, S_max) and
 //   F o G = (aF aG, aF cG + cF, clamp(aF loG + cF, loF, hiF), clamp(aF hiG + cF, loF, hiF)).
-// The segment is scanned 32 events at a time; the pixel's events of each group
-// are compacted to the low lanes (arrival order), their maps are combined by a
-// warp-shuffle inclusive scan, and the last prefix is applied to the state.
+// The pixel's events are compacted from the segment into the warp's staging
+// (arrival order) 32 at a time, their maps are combined by a warp-shuffle
+// inclusive scan, and the last prefix is applied to the state.
 template <int BM>
 __device__ __forceinline__ void dense_pixel_apply(float* S, float* T, const uint2* sub, uint2* stage, int e0,
                                                   int e1, int q, uint32_t trel, int lane, const FastConst& k) {
   float s = S[q], tprev = T[q];
-  for (int base = e0; base < e1; base += 32) {
-    const int i = base + lane;
-    const uint2 ev = i < e1 ? sub[i] : make_uint2(0u, 0xffffffffu);
-    const bool mine = i < e1 && (int)(ev.y & 0x7fffffffu) == q;
-    const unsigned m = __ballot_sync(kFull, mine);
-    if (!m) continue;
-    const int nk = __popc(m);
-    if (mine) stage[__popc(m & lanemask_lt())] = ev;     // compact, arrival order kept
+  int base = e0, cnt = 0;                                   // segment position; compacted events in stage
+  while (true) {
+    // compact the pixel's events (arrival order) until 32 are staged or the segment ends:
+    // a segment of a few dozen events with ~10 of the pixel's costs one scan, not one per 32
+    while (cnt < 32 && base < e1) {
+      const int i = base + lane;
+      const uint2 ev = i < e1 ? sub[i] : make_uint2(0u, 0xffffffffu);
+      const bool mine = i < e1 && (int)(ev.y & 0x7fffffffu) == q;
+      const unsigned m = __ballot_sync(kFull, mine);
+      if (mine) stage[cnt + __popc(m & lanemask_lt())] = ev;   // cnt + 32 <= 64 <= kStage
+      cnt += __popc(m);
+      base += 32;
+    }
+    if (cnt == 0) break;
     __syncwarp();
+    const int nk = min(cnt, 32);
     const uint2 cev = stage[lane];
+    const uint2 rest = stage[32 + lane];
     __syncwarp();
+    if (lane < cnt - nk) stage[lane] = rest;               // the overflow moves to the front
+    cnt -= nk;
     const float te = (float)(int32_t)(cev.x - trel);
     float tp = __shfl_up_sync(kFull, te, 1);
     if (lane == 0) tp = tprev;
@@ -170,6 +180,7 @@ __device__ __forceinline__ void dense_pixel_apply(float* S, float* T, const uint
     const float Llo = __shfl_sync(kFull, flo, nk - 1), Lhi = __shfl_sync(kFull, fhi, nk - 1);
     s = fminf(fmaxf(fmaf(La, s, Lc), Llo), Lhi);
     tprev = __shfl_sync(kFull, te, nk - 1);
+    __syncwarp();
   }
   if (lane == 0) {
     S[q] = s;
