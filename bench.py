@@ -133,7 +133,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -146,6 +146,10 @@ class ClockSampler:
 
     def mark(self, t0, t1):
         self.window = (t0, t1)
+
+    def in_window(self):
+        t0, t1 = getattr(self, "window", (0, 1e30))
+        return sum(1 for ts, _ in self.lines if t0 <= ts <= t1 + 0.15)
 
     def __exit__(self, *a):
         if self.proc:
@@ -311,6 +315,12 @@ def run_streams(args, ctx, peaks, handle_factory=None, stream_factory=None):
         ms_total = ctx.timed(step, args.steps, stream)
         clk.mark(t_wall0, time.time())
         stats = e.last_render_stats()
+        # a short timed region (20 x 4 ms) may fall between two nvidia-smi samples (20 ms
+        # apart, delivered late): keep the GPU on the same step until two samples are in
+        t_busy = time.time()
+        while cuda and clk.proc is not None and clk.in_window() < 2 and time.time() - t_busy < 1.0:
+            step()
+            torch.cuda.synchronize()
         # Per-kernel launch durations: a separate pass with a CUDA event pair around
         # every launch (they serialise the K1/K2 overlap, so not in the timed region).
         kt_steps = 0 if args.no_kernel_timing else max(1, min(args.steps, 3))
