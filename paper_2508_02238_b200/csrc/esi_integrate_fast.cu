@@ -33,7 +33,10 @@ namespace {
 #endif
 constexpr int kNW = ESI_K2_WARPS;             // warps per CTA
 constexpr int kNT = kNW * 32;                 // threads per CTA
-constexpr int kEPT = (kK2Ctas >= 4 ? 1024 : 1536) / kNT;   // events per thread per segment (smem budget)
+#ifndef ESI_K2_SB
+#define ESI_K2_SB (kK2Ctas >= 4 ? 1024 : 1536)
+#endif
+constexpr int kEPT = ESI_K2_SB / kNT;          // events per thread per segment (smem budget)
 constexpr int kSB = kNT * kEPT;               // events per sub-batch
 constexpr int kStage = (kEPT * 32 + 1) / 2 > 64 ? (kEPT * 32 + 1) / 2 : 64;   // uint2 per warp: kEPT * 32 chain heads (u32), >= 64 for the dense compaction
 constexpr int kWinCap = 32;                   // window ends listed per pass (warp 0, per sub-batch)

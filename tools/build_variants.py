@@ -6,6 +6,9 @@ VARIANTS = {
     "k2c4": ["-DESI_K2_CTAS=4"],
     "k2c2w12": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=12"],
     "k2c2w16": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=16"],
+    "k2c2w12sb3072": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=12", "-DESI_K2_SB=3072"],
+    "k2c2w8sb3072": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=8", "-DESI_K2_SB=3072"],
+    "k2c2w16sb3072": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=16", "-DESI_K2_SB=3072"],
     "k2c2": ["-DESI_K2_CTAS=2"],
     "k2c2_t2048": ["-DESI_K2_CTAS=2", "-DESI_TILE=2048", "-DESI_PART_THREADS=256", "-DESI_PART_CTAS=2"],
     "t2048c3": ["-DESI_TILE=2048", "-DESI_PART_THREADS=256", "-DESI_PART_CTAS=3"],
