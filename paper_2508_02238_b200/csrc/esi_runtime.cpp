@@ -170,7 +170,7 @@ int ensure_pinned(esi_handle_t* h, size_t bytes) {
   if (bytes <= h->h_pin_cap) return ESI_OK;
   if (h->h_pin) cudaFreeHost(h->h_pin);
   h->h_pin = nullptr;
-  size_t cap = std::max<size_t>(bytes, 4096);
+  size_t cap = std::max<size_t>(std::max(bytes, 2 * h->h_pin_cap), 4096);   // geometric growth
   if (cudaMallocHost((void**)&h->h_pin, cap) != cudaSuccess) {
     cudaGetLastError();
     h->h_pin_cap = 0;
@@ -185,7 +185,7 @@ int ensure_dev(esi_handle_t* h, T** p, size_t* cap, size_t n) {
   if (n <= *cap) return ESI_OK;
   if (*p) cudaFree((void*)*p);
   *p = nullptr;
-  size_t c = std::max<size_t>(n, 64);
+  size_t c = std::max<size_t>(std::max(n, 2 * *cap), 64);   // geometric growth: few reallocations
   if (cudaMalloc((void**)p, c * sizeof(T)) != cudaSuccess) {
     cudaGetLastError();
     *cap = 0;
@@ -206,12 +206,21 @@ void* pool_take(esi_handle_t* h, size_t bytes, size_t* got) {
     h->pool.erase(h->pool.begin() + bi);
     return p;
   }
+  // new buffers are rounded up to a power of two (>= 1 MiB), so that a stream of
+  // packets of slowly varying size reuses them instead of calling cudaMalloc
+  // (which synchronises the device) for every packet a few events larger
+  size_t want = (size_t)1 << 20;
+  while (want < bytes) want <<= 1;
   void* p = nullptr;
-  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+  if (cudaMalloc(&p, want) != cudaSuccess) {
     cudaGetLastError();
-    return nullptr;
+    if (want == bytes || cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    want = bytes;
   }
-  *got = bytes;
+  *got = want;
   return p;
 }
 
