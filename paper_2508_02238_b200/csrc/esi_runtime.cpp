@@ -1249,7 +1249,8 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     ia.nb = h->nb;
     ia.dp = h->dp;
     ia.mp = h->mp;
-    e = launch_partition(pa, n_tiles, h->rank_mode, st);
+    e = cudaMemsetAsync(h->tile_ctr, 0, 2 * sizeof(uint32_t), st);   // K1 work counters
+    if (e == cudaSuccess) e = launch_partition(pa, n_tiles, h->rank_mode, st);
     if (e == cudaSuccess) e = launch_slice_summary(ia, t01[0], maps, h->allow_fast ? 1 : 0, st);
     if (e != cudaSuccess) fail(cuda_fail(h, e));
   }
@@ -1322,6 +1323,7 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   pa.wide_t = h->wide_t[0];
   pa.err = h->d_err;
   ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), h->stream));
+  ESI_CUDA(h, cudaMemsetAsync(h->tile_ctr, 0, 2 * sizeof(uint32_t), h->stream));   // K1 work counters
   ESI_CUDA(h, launch_partition(pa, n_tiles, h->rank_mode, h->stream));
   std::vector<uint2> rec(n_tiles * (size_t)kTile);
   std::vector<uint32_t> meta((size_t)h->nb * n_tiles);
