@@ -202,11 +202,14 @@ def destroy(h: int) -> None:
     _lib().esi_destroy(h)
 
 
-def frame_metrics(frames, truth, device: int = 0):
+def frame_metrics(frames, truth, device: Optional[int] = None):
     """SPEC metrics on the GPU (esi_frame_metrics): frames [F, H, W]
-    uint8 and truth [H, W] or [F, H, W] float32 log intensity, both CUDA tensors.
+    uint8 and truth [H, W] or [F, H, W] float32 log intensity, both CUDA tensors
+    (on `device`, default: the frames' device).
     Returns (pearson[F], mse_norm[F]) as numpy float64 (NaN = missing)."""
     import torch
+    if device is None:
+        device = frames.device.index if frames.device.index is not None else torch.cuda.current_device()
     F = frames.shape[0]
     P = frames[0].numel()
     per = 1 if truth.dim() == 3 else 0
@@ -224,6 +227,15 @@ class Esi:
     def __init__(self, width: int, height: int, **params):
         self.W, self.H = int(width), int(height)
         self.P = self.W * self.H
+        if "device" not in params:
+            # the handle lives on the caller's current CUDA device (one process per GPU:
+            # torch.cuda.set_device(local_rank)), not on device 0
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    params = dict(params, device=torch.cuda.current_device())
+            except ImportError:
+                pass
         self.params = default_params(**params)
         self.h = create(self.W, self.H, self.params)
         self._borrowed = []          # (buffer, cumulative end): borrowed buffers kept alive until consumed

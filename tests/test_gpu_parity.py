@@ -193,6 +193,24 @@ def test_render_many_equals_repeated_render_within_tolerance():
     assert_state_close(Sa, Ta, Sb.astype(np.float64), Tb)
 
 
+def test_handle_lives_on_the_current_cuda_device():
+    """One process per GPU (torch.cuda.set_device(local_rank)): an Esi handle
+    created without an explicit device uses the caller's current device, not
+    device 0 (bench.py / dist.py create their handles this way)."""
+    from paper_2508_02238_b200 import Esi
+    dev = torch.cuda.current_device()
+    e = Esi(64, 48)
+    try:
+        assert e.params.device == dev
+    finally:
+        e.close()
+    e = Esi(64, 48, device=dev)
+    try:
+        assert e.params.device == dev
+    finally:
+        e.close()
+
+
 def test_interleaved_push_render_and_host_paths():
     from paper_2508_02238_b200 import Esi
     ev = random_stream(13, 30, 20, 50_000, 500_000)
