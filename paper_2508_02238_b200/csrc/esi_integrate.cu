@@ -23,6 +23,7 @@
 // Frame j is rendered in the chunk c with t_first(c) <= t_j < t_first(c+1), so
 // all events with t <= t_j have been integrated (ties belong to the frame,
 // reading A6) and none later.
+#include <atomic>
 #include "esi_device.cuh"
 
 namespace esi {
@@ -279,12 +280,12 @@ static cudaError_t launch_nw(const IntArgs& a, cudaStream_t s) {
   const size_t smem = integrate_smem_bytes(NW * kWarpPx);
   int dev = 0;
   cudaGetDevice(&dev);
-  static int configured[64] = {0};   // per device (the attribute is per context)
-  if (dev < 0 || dev >= 64 || !configured[dev]) {
+  static std::atomic<int> configured[64];   // zero-initialised; set-once flags (idempotent, race-free)   // per device (the attribute is per context)
+  if (dev < 0 || dev >= 64 || !configured[dev].load(std::memory_order_relaxed)) {
     cudaError_t e = cudaFuncSetAttribute(esi_integrate_wide_kernel<NW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) configured[dev] = 1;
+    if (dev >= 0 && dev < 64) configured[dev].store(1, std::memory_order_relaxed);
   }
   esi_integrate_wide_kernel<NW><<<a.nb, NW * 32, smem, s>>>(a);
   return cudaGetLastError();

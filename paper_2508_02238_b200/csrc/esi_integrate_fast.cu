@@ -20,6 +20,7 @@
 //   u = k_us * ((tau_h - dt) + tau_l),  d = max(u, 0)^b
 // (tau_h - dt is exact near the cutoff, so u keeps full relative precision and
 // u <= 0 exactly when dt >= dt_cut = ceil(tau)).
+#include <atomic>
 #include "esi_device.cuh"
 
 namespace esi {
@@ -377,13 +378,13 @@ cudaError_t launch_fast_b(const IntArgs& a, cudaStream_t s) {
   const size_t smem = fast_smem_bytes(a.band_px, a.n_tiles);
   int dev = 0;
   cudaGetDevice(&dev);
-  static int configured[64] = {0};   // per device (the attribute is per context)
-  if (dev < 0 || dev >= 64 || !configured[dev]) {
+  static std::atomic<int> configured[64];   // zero-initialised; set-once flags (idempotent, race-free)   // per device (the attribute is per context)
+  if (dev < 0 || dev >= 64 || !configured[dev].load(std::memory_order_relaxed)) {
     const size_t mx = fast_smem_bytes(kMaxBandPx, kMaxTilesPerChunk);
     cudaError_t e = cudaFuncSetAttribute(esi_integrate_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)mx);
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) configured[dev] = 1;
+    if (dev >= 0 && dev < 64) configured[dev].store(1, std::memory_order_relaxed);
   }
   esi_integrate_kernel<BM><<<a.nb, kNT, smem, s>>>(a);
   return cudaGetLastError();

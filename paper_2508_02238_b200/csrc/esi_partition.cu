@@ -17,6 +17,7 @@
 // Record (8 B): x = low 32 bits of t, y = pixel-in-band | (p < 0) << 31.
 // meta[band][tile] = offset-in-tile | count << 16 tells K2 where its events are.
 #include <algorithm>
+#include <atomic>
 #include "esi_device.cuh"
 
 namespace esi {
@@ -324,25 +325,28 @@ static cudaError_t launch_part_t(const PartArgs& a, int n_tiles, cudaStream_t s)
   const size_t smem = partition_smem_bytes(a.nb, RA);
   int dev = 0;
   cudaGetDevice(&dev);
-  static int configured[64] = {0};   // per device (the attribute is per context); the maximum once
-  static int n_sm[64] = {0};
-  static int occ[64][2] = {{0}};      // resident CTAs per SM for band count occ[.][1]
+  static std::atomic<int> configured[64];   // zero-initialised; set-once flags (idempotent, race-free)   // per device (the attribute is per context); the maximum once
+  static std::atomic<int> n_sm[64];
+  static std::atomic<uint64_t> occ[64];   // (band count << 32) | resident CTAs per SM
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!configured[dev]) {
+  if (!configured[dev].load(std::memory_order_acquire)) {
+    int nsm = 0;
     cudaError_t e = cudaFuncSetAttribute(esi_partition_kernel<RA, V, B32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)partition_smem_bytes(kMaxBands, RA));
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    configured[dev] = 1;
+    n_sm[dev].store(nsm, std::memory_order_relaxed);
+    configured[dev].store(1, std::memory_order_release);
   }
-  if (occ[dev][1] != a.nb || occ[dev][0] <= 0) {
+  uint64_t oc = occ[dev].load(std::memory_order_relaxed);
+  if ((oc >> 32) != (uint64_t)(uint32_t)a.nb || (oc & 0xffffffffu) == 0) {
     int o = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, esi_partition_kernel<RA, V, B32>, kPartThreads, smem);
     if (e != cudaSuccess) return e;
-    occ[dev][0] = o > 0 ? o : 1;
-    occ[dev][1] = a.nb;
+    oc = ((uint64_t)(uint32_t)a.nb << 32) | (uint32_t)(o > 0 ? o : 1);
+    occ[dev].store(oc, std::memory_order_relaxed);
   }
-  const int grid = (int)std::min<int64_t>(n_tiles, (int64_t)occ[dev][0] * n_sm[dev]);   // persistent CTAs
+  const int grid = (int)std::min<int64_t>(n_tiles, (int64_t)(oc & 0xffffffffu) * n_sm[dev].load(std::memory_order_relaxed));   // persistent CTAs
   PartArgs b = a;
   b.n_tiles = n_tiles;
   esi_partition_kernel<RA, V, B32><<<grid, kPartThreads, smem, s>>>(b);

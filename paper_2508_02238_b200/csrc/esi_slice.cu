@@ -20,6 +20,7 @@
 //   run's events into the pixel's summary (shared memory for the chunk).
 // K6 esi_slice_compose_kernel / K7 esi_slice_apply_kernel: elementwise over pixels.
 #include <algorithm>
+#include <atomic>
 #include "esi_device.cuh"
 
 namespace esi {
@@ -298,12 +299,12 @@ cudaError_t launch_slice_summary_b(const IntArgs& a, int64_t tbase, esi_slice_ma
   const size_t smem = sl_smem_bytes(a.band_px, a.n_tiles);
   int dev = 0;
   cudaGetDevice(&dev);
-  static int configured[64] = {0};
-  if (dev < 0 || dev >= 64 || !configured[dev]) {
+  static std::atomic<int> configured[64];   // zero-initialised; set-once flags (idempotent, race-free)
+  if (dev < 0 || dev >= 64 || !configured[dev].load(std::memory_order_relaxed)) {
     cudaError_t e = cudaFuncSetAttribute(esi_slice_summary_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sl_smem_bytes(kMaxBandPx, kMaxTilesPerChunk));
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) configured[dev] = 1;
+    if (dev >= 0 && dev < 64) configured[dev].store(1, std::memory_order_relaxed);
   }
   esi_slice_summary_kernel<BM><<<a.nb, kST, smem, s>>>(a, tbase, maps);
   return cudaGetLastError();
