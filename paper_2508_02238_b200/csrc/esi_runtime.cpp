@@ -1207,14 +1207,26 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     if (e != cudaSuccess) fail(cuda_fail(h, e));
     else if (herr != kNoError) fail((int)(herr & 0xff));
   }
-  for (int64_t o = 0; !rc && o < (int64_t)n; o += h->chunk_events) {
-    const int64_t nc = std::min<int64_t>(h->chunk_events, (int64_t)n - o);
-    int64_t t01[2];
-    cudaError_t e = cudaMemcpyAsync(&t01[0], &ev[o].t_us, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&t01[1], &ev[o + nc - 1].t_us, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  // every chunk's first and last time, read back at once (one sync, not one per chunk)
+  const int64_t n_chunks = ((int64_t)n + h->chunk_events - 1) / h->chunk_events;
+  std::vector<int64_t> t01((size_t)(2 * n_chunks));
+  if (!rc) rc = ensure_pinned(h, (size_t)(2 * n_chunks) * sizeof(int64_t));
+  if (!rc) {
+    int64_t* ht = (int64_t*)h->h_pin;
+    cudaError_t e = cudaSuccess;
+    for (int64_t c = 0; c < n_chunks && e == cudaSuccess; ++c) {
+      const int64_t o = c * h->chunk_events, nc = std::min<int64_t>(h->chunk_events, (int64_t)n - o);
+      e = cudaMemcpyAsync(ht + 2 * c, &ev[o].t_us, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(ht + 2 * c + 1, &ev[o + nc - 1].t_us, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) { fail(cuda_fail(h, e)); break; }
-    if (t01[1] - t01[0] >= ((int64_t)1 << 31)) { fail(ESI_ERR_INVALID_ARG); break; }
+    if (e != cudaSuccess) fail(cuda_fail(h, e));
+    else std::copy(ht, ht + 2 * n_chunks, t01.begin());
+  }
+  for (int64_t o = 0, c = 0; !rc && o < (int64_t)n; o += h->chunk_events, ++c) {
+    const int64_t nc = std::min<int64_t>(h->chunk_events, (int64_t)n - o);
+    if (t01[2 * c + 1] - t01[2 * c] >= ((int64_t)1 << 31)) { fail(ESI_ERR_INVALID_ARG); break; }
+    cudaError_t e = cudaSuccess;
     const int n_tiles = (int)((nc + kTile - 1) / kTile);
     PartArgs pa;
     pa.ev = ev + o;
@@ -1251,7 +1263,7 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     ia.mp = h->mp;
     e = cudaMemsetAsync(h->tile_ctr, 0, 2 * sizeof(uint32_t), st);   // K1 work counters
     if (e == cudaSuccess) e = launch_partition(pa, n_tiles, h->rank_mode, st);
-    if (e == cudaSuccess) e = launch_slice_summary(ia, t01[0], maps, h->allow_fast ? 1 : 0, st);
+    if (e == cudaSuccess) e = launch_slice_summary(ia, t01[2 * c], maps, h->allow_fast ? 1 : 0, st);
     if (e != cudaSuccess) fail(cuda_fail(h, e));
   }
   if (!rc) {
