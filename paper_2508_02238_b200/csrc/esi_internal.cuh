@@ -152,6 +152,7 @@ struct IntArgs {
   MapParams mp;
   WideParams wp;
   const unsigned long long* gate;    // non-null: exit without writing if *gate != kNoError
+  int32_t atomic_rank;               // warp-wide shared atomics serve lanes in lane order (probed)
 };
 
 struct ReadoutArgs {

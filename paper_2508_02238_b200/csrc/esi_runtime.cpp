@@ -1261,6 +1261,7 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     ia.nb = h->nb;
     ia.dp = h->dp;
     ia.mp = h->mp;
+    ia.atomic_rank = h->rank_mode == 1 ? 1 : 0;   // K5's ranks follow K1's (probed) mode
     e = cudaMemsetAsync(h->tile_ctr, 0, 2 * sizeof(uint32_t), st);   // K1 work counters
     if (e == cudaSuccess) e = launch_partition(pa, n_tiles, h->rank_mode, st);
     if (e == cudaSuccess) e = launch_slice_summary(ia, t01[2 * c], maps, h->allow_fast ? 1 : 0, st);

@@ -117,8 +117,9 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
     __syncthreads();                                       // pass gathered; previous pass done
     if (sb0 + kSE < n_b) gather_sub<kSE>(a.rec, pre, mo, n_tiles, n_b, sb0 + kSE, ss.buf[(kb & 1) ^ 1], warp, kSW, lane);
 
-    // rank: a pixel's events of one warp round are ordered by lane (match.any), the
-    // rounds of a warp share in program order, the shares by warp: stable
+    // rank: a pixel's events of one warp round are ordered by lane (lane-ordered
+    // atomics when probed, else match.any), the rounds of a warp share in program
+    // order, the shares by warp: stable
     uint32_t evt[kRounds], key[kRounds];
     const int s0 = warp * kShare;
     uint32_t* h32 = reinterpret_cast<uint32_t*>(h8 + warp * bp);
@@ -129,24 +130,31 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
       const unsigned am = __ballot_sync(kFull, act);
       if (am == 0u) break;
       uint32_t px = 0u, sgn = 0u;
-      unsigned peers = 0u;
       if (act) {
         const uint2 e = cur[s0 + si];
         evt[r] = e.x;
         px = e.y & 0x7fffffffu;
         sgn = e.y & 0x80000000u;
         ESI_DCHECK(px < (uint32_t)npx);
-        peers = __match_any_sync(am, px);
       }
-      const int leader = act ? __ffs(peers) - 1 : lane;
-      uint32_t base = 0u;
-      if (act && leader == lane) {
-        const uint32_t sh = (px & 3u) * 8u;
-        const uint32_t old = atomicAdd(h32 + (px >> 2), (uint32_t)__popc(peers) << sh);
-        base = (old >> sh) & 0xffu;
+      const uint32_t sh = (px & 3u) * 8u;
+      if (a.atomic_rank) {
+        // lane-ordered shared atomics (probed at esi_create, as K1's default): each
+        // lane's old count is its rank among the round's lanes of its pixel
+        const uint32_t old = act ? atomicAdd(h32 + (px >> 2), 1u << sh) : 0u;
+        key[r] = px | (((old >> sh) & 0xffu) << 12) | sgn;
+      } else {
+        unsigned peers = 0u;
+        if (act) peers = __match_any_sync(am, px);
+        const int leader = act ? __ffs(peers) - 1 : lane;
+        uint32_t base = 0u;
+        if (act && leader == lane) {
+          const uint32_t old = atomicAdd(h32 + (px >> 2), (uint32_t)__popc(peers) << sh);
+          base = (old >> sh) & 0xffu;
+        }
+        base = __shfl_sync(kFull, base, leader);
+        key[r] = px | ((base + (uint32_t)__popc(peers & lanemask_lt())) << 12) | sgn;
       }
-      base = __shfl_sync(kFull, base, leader);
-      key[r] = px | ((base + (uint32_t)__popc(peers & lanemask_lt())) << 12) | sgn;
     }
     __syncthreads();
     // offsets: per-pixel totals over the warps, block-wide exclusive scan
