@@ -29,6 +29,7 @@ namespace {
 
 constexpr int kSW = 8;                        // warps per CTA
 constexpr int kST = kSW * 32;
+static_assert(kSW == 8, "per-pixel warp counts are 8 bytes (dp4a prefix sums)");
 constexpr int kShare = 255;                   // events per warp share (u8 per-warp pixel counts)
 constexpr int kSE = kSW * kShare;             // events per pass (2040)
 constexpr int kRounds = (kShare + 31) / 32;
@@ -64,7 +65,7 @@ struct SliceStatic {
 };
 
 __host__ __device__ inline size_t r16s(size_t b) { return (b + 15) & ~(size_t)15; }
-// dynamic: h8[kSW][bp], off[bp + 1], pre[n_tiles + 1], mo[n_tiles]; the summaries
+// dynamic: h8[bp][kSW], off[bp + 1], pre[n_tiles + 1], mo[n_tiles]; the summaries
 // themselves stay in global memory (L2): a pixel's map is read and written once
 // per pass by the thread that folds its run, which keeps the CTA at 67 KB of shared
 // memory (3 CTAs per SM, one wave of bands)
@@ -122,7 +123,9 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
     // order, the shares by warp: stable
     uint32_t evt[kRounds], key[kRounds];
     const int s0 = warp * kShare;
-    uint32_t* h32 = reinterpret_cast<uint32_t*>(h8 + warp * bp);
+    // per-pixel counts of each warp's share, laid out [pixel][warp] (8 bytes per pixel)
+    uint32_t* h32 = reinterpret_cast<uint32_t*>(h8) + (warp >> 2);
+    const uint32_t wsh = (uint32_t)(warp & 3) * 8u;
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
       const int si = r * 32 + lane;
@@ -137,20 +140,19 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
         sgn = e.y & 0x80000000u;
         ESI_DCHECK(px < (uint32_t)npx);
       }
-      const uint32_t sh = (px & 3u) * 8u;
       if (a.atomic_rank) {
         // lane-ordered shared atomics (probed at esi_create, as K1's default): each
         // lane's old count is its rank among the round's lanes of its pixel
-        const uint32_t old = act ? atomicAdd(h32 + (px >> 2), 1u << sh) : 0u;
-        key[r] = px | (((old >> sh) & 0xffu) << 12) | sgn;
+        const uint32_t old = act ? atomicAdd(h32 + 2 * px, 1u << wsh) : 0u;
+        key[r] = px | (((old >> wsh) & 0xffu) << 12) | sgn;
       } else {
         unsigned peers = 0u;
         if (act) peers = __match_any_sync(am, px);
         const int leader = act ? __ffs(peers) - 1 : lane;
         uint32_t base = 0u;
         if (act && leader == lane) {
-          const uint32_t old = atomicAdd(h32 + (px >> 2), (uint32_t)__popc(peers) << sh);
-          base = (old >> sh) & 0xffu;
+          const uint32_t old = atomicAdd(h32 + 2 * px, (uint32_t)__popc(peers) << wsh);
+          base = (old >> wsh) & 0xffu;
         }
         base = __shfl_sync(kFull, base, leader);
         key[r] = px | ((base + (uint32_t)__popc(peers & lanemask_lt())) << 12) | sgn;
@@ -162,18 +164,19 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
       const int ng = bp >> 2;
       const int gpt = (ng + kST - 1) / kST;
       const int g0 = tid * gpt;
-      uint32_t ev4[4], od4[4], local = 0u;
+      uint32_t cnt[4][4], local = 0u;                   // pixel totals: the 8 warp bytes summed (dp4a)
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        ev4[g] = od4[g] = 0u;
-        if (g < gpt && g0 + g < ng) {
 #pragma unroll
-          for (int w = 0; w < kSW; ++w) {
-            const uint32_t v = reinterpret_cast<const uint32_t*>(h8 + w * bp)[g0 + g];
-            ev4[g] += v & 0x00ff00ffu;
-            od4[g] += (v >> 8) & 0x00ff00ffu;
-          }
-          local += (ev4[g] & 0xffffu) + (ev4[g] >> 16) + (od4[g] & 0xffffu) + (od4[g] >> 16);
+        for (int u = 0; u < 4; ++u) cnt[g][u] = 0u;
+        if (g < gpt && g0 + g < ng) {
+          const uint4 va = *reinterpret_cast<const uint4*>(h8 + 32 * (g0 + g));
+          const uint4 vb = *reinterpret_cast<const uint4*>(h8 + 32 * (g0 + g) + 16);
+          cnt[g][0] = __dp4a(va.x, 0x01010101u, __dp4a(va.y, 0x01010101u, 0u));
+          cnt[g][1] = __dp4a(va.z, 0x01010101u, __dp4a(va.w, 0x01010101u, 0u));
+          cnt[g][2] = __dp4a(vb.x, 0x01010101u, __dp4a(vb.y, 0x01010101u, 0u));
+          cnt[g][3] = __dp4a(vb.z, 0x01010101u, __dp4a(vb.w, 0x01010101u, 0u));
+          local += cnt[g][0] + cnt[g][1] + cnt[g][2] + cnt[g][3];
         }
       }
       uint32_t x = local;
@@ -192,10 +195,10 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
       for (int g = 0; g < 4; ++g) {
         if (g < gpt && g0 + g < ng) {
           uint16_t* o = off + 4 * (g0 + g);
-          o[0] = (uint16_t)run; run += ev4[g] & 0xffffu;
-          o[1] = (uint16_t)run; run += od4[g] & 0xffffu;
-          o[2] = (uint16_t)run; run += ev4[g] >> 16;
-          o[3] = (uint16_t)run; run += od4[g] >> 16;
+          o[0] = (uint16_t)run; run += cnt[g][0];
+          o[1] = (uint16_t)run; run += cnt[g][1];
+          o[2] = (uint16_t)run; run += cnt[g][2];
+          o[3] = (uint16_t)run; run += cnt[g][3];
         }
       }
       if (tid == kST - 1) off[bp] = (uint16_t)n;
@@ -207,8 +210,13 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
       const int si = r * 32 + lane;
       if (!(si < kShare && s0 + si < n)) break;
       const uint32_t px = key[r] & 0xfffu;
-      uint32_t pos = (uint32_t)off[px] + ((key[r] >> 12) & 0xffu);
-      for (int w = 0; w < warp; ++w) pos += h8[w * bp + px];
+      // + the events of this pixel in the shares of warps < warp: the low bytes of
+      // the pixel's 8 counts, summed by dp4a
+      const uint2 v = *reinterpret_cast<const uint2*>(h8 + 8 * px);
+      const uint32_t mA = warp >= 4 ? 0xffffffffu : ((1u << (8 * warp)) - 1u);
+      const uint32_t mB = warp > 4 ? ((1u << (8 * (warp - 4))) - 1u) : 0u;
+      const uint32_t pos = (uint32_t)off[px] + ((key[r] >> 12) & 0xffu) +
+                           __dp4a(v.x & mA, 0x01010101u, __dp4a(v.y & mB, 0x01010101u, 0u));
       ESI_DCHECK(pos < (uint32_t)n);
       cur[pos] = make_uint2(evt[r], px | (key[r] & 0x80000000u));
     }
