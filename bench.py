@@ -259,7 +259,14 @@ def make_stream(name, rank, idx, args):
     from esi_synth import make_workload
     if name == "c4":
         seed = 4 + 1000 * rank + idx          # rank 0 = the c4 stream; other ranks: independent streams
-        return make_workload("c4", "cuda", seed=seed, fps=args.fps)
+        w = make_workload("c4", "cuda", seed=seed, fps=args.fps)
+        if getattr(args, "roi", None):        # local activity: keep only the events inside a rectangle
+            x0, y0, x1, y1 = (float(v) for v in args.roi.split(","))
+            xy = w.events[:, 1]
+            x, y = xy & 0xffff, (xy >> 16) & 0xffff
+            keep = (x >= int(x0 * w.W)) & (x < int(x1 * w.W)) & (y >= int(y0 * w.H)) & (y < int(y1 * w.H))
+            w.events = w.events[keep].contiguous()
+        return w
     seed = 5000 + 64 * rank + idx
     return make_workload("c5a", "cuda", seed=seed)
 
@@ -661,6 +668,9 @@ def parse_args(argv):
     ap.add_argument("--impl", default="esi", choices=["esi", "reference"])
     ap.add_argument("--config", default="c4", choices=["c4", "c5a", "c5b", "c4t"])
     ap.add_argument("--fps", type=int, default=100)
+    ap.add_argument("--roi", default=None,
+                    help="c4 only: x0,y0,x1,y1 as fractions of the sensor; events outside are dropped "
+                         "(a locally active scene; not the BASELINE workload)")
     ap.add_argument("--validation", default="push", choices=["push", "fused"],
                     help="push: validate_on_push=1 (the library default, atomic push); fused: checks in K1")
     ap.add_argument("--e2e-steps", type=int, default=2)

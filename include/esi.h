@@ -95,7 +95,19 @@ typedef struct {
    * states are unbounded sums that can cancel, so they accumulate in fp64
    * (the wide kernel; S is stored in fp32 between chunks). */
   int32_t state_unclamped;
+  /* How pixel ids map to the integrate kernel's bands (one CTA each; esi_layout).
+   * A performance knob only: frames and state do not depend on it.
+   * ESI_BANDS_CONTIGUOUS (0, default): band b = a run of band_px consecutive ids
+   *   (fastest when the activity covers the sensor, as in BASELINE's configs).
+   * ESI_BANDS_INTERLEAVED (1): ids are dealt to the bands in groups of 64
+   *   consecutive ids, round-robin -- every band samples the whole sensor, so the
+   *   bands stay balanced when the activity is local (a moving object);
+   *   measured in DESIGN.md section 7e. */
+  int32_t band_layout;
 } esi_params_t;
+
+#define ESI_BANDS_CONTIGUOUS 0
+#define ESI_BANDS_INTERLEAVED 1
 
 typedef struct esi_handle esi_handle_t;
 
@@ -286,13 +298,15 @@ int esi_last_render_stats(esi_handle_t* h, int64_t* kernel_launches, int64_t* ev
                           int64_t* chunks);
 
 /* The handle's band layout: bands (K1 partition buckets = integrate CTAs),
- * pixels per band, warps per integrate CTA.  Any pointer may be NULL. */
+ * pixel slots per band, warps per integrate CTA.  With params.band_layout =
+ * ESI_BANDS_INTERLEAVED pixel id q belongs to band (q / 64) % n_bands, with
+ * ESI_BANDS_CONTIGUOUS to band q / band_px.  Any pointer may be NULL. */
 int esi_layout(esi_handle_t* h, int32_t* n_bands, int32_t* band_px, int32_t* warps_per_band);
 
 /* Debug export of the bit-exact grouping step: runs only the
  * ingest/partition kernel over the pending events of the first chunk and
- * copies back, for every band (a run of band_px consecutive pixel ids), the
- * events routed to it in arrival order, as records {t_us, pixel id, p}.
+ * copies back, for every band (esi_layout), the events routed to it in arrival order, as records
+ * {t_us, pixel id, p}.
  * out_* must hold n_out entries; band_start[nb+1] receives the CSR offsets.
  * Does not consume events. */
 int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8_t* out_p,

@@ -68,7 +68,7 @@ __device__ __forceinline__ uint32_t wide_map8(double v, const WideParams& wp) {
 
 template <int NW>
 __device__ __forceinline__ void warp_readout(const IntArgs& a, const IntCtx<NW>& c, int j,
-                                             int64_t px0, int npx, int warp, int lane) {
+                                             int band, int npx, int warp, int lane) {
   const int base = warp * kWarpPx + lane * 8;
   if (base >= npx) return;
   const int64_t tj = a.tf[j];
@@ -79,7 +79,7 @@ __device__ __forceinline__ void warp_readout(const IntArgs& a, const IntCtx<NW>&
     if (a.wp.readout_decay) v *= wide_decay(tj - c.Tsm[base + q], a.wp);
     bytes[q] = wide_map8(v, a.wp);
   }
-  uint8_t* dst = a.out + (int64_t)j * a.P + px0 + base;
+  uint8_t* dst = a.out + (int64_t)j * a.P + band_gpix(a.bm, band, base);   // 8 pixels never straddle a 64-pixel group
   if (a.vec8 && base + 8 <= npx) {
     const uint32_t lo = bytes[0] | (bytes[1] << 8) | (bytes[2] << 16) | (bytes[3] << 24);
     const uint32_t hi = bytes[4] | (bytes[5] << 8) | (bytes[6] << 16) | (bytes[7] << 24);
@@ -109,8 +109,7 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
 
   const int band = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t px0 = (int64_t)band * a.band_px;            // band_px <= BP
-  const int npx = (int)min((int64_t)a.band_px, a.P - px0);
+  const int npx = band_npx(a.bm, band, a.P);                // interleaved bands (esi_internal.cuh); band_px <= BP
 
   if (a.gate && *a.gate != kNoError) return;   // lazy validation found an invalid event: write nothing
   const ChunkInfo ci = *a.info;
@@ -123,8 +122,9 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
 
   for (int i = threadIdx.x; i < BP; i += NT) {
     const bool in = i < npx;
-    c.Ssm[i] = in ? (double)a.S[px0 + i] : 0.0;
-    c.Tsm[i] = in ? a.T[px0 + i] : 0;
+    const int64_t g = band_gpix(a.bm, band, i);
+    c.Ssm[i] = in ? (double)a.S[g] : 0.0;
+    c.Tsm[i] = in ? a.T[g] : 0;
     c.tag[i] = 32;
   }
   int n_b = 0;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
       i += nv;
       if (nv < m) {
         if (j < f_hi) {
-          warp_readout<NW>(a, c, j, px0, npx, warp, lane);
+          warp_readout<NW>(a, c, j, band, npx, warp, lane);
           ++j;
         } else {
           done = true;  // the rest is later than the last frame: stays pending
@@ -257,20 +257,21 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
     }
     // 4. frames whose events are all in this or earlier sub-batches
     while (j < f_hi && a.tf[j] < tnext) {
-      warp_readout<NW>(a, c, j, px0, npx, warp, lane);
+      warp_readout<NW>(a, c, j, band, npx, warp, lane);
       ++j;
     }
     __syncthreads();
   }
   while (j < f_hi) {
-    warp_readout<NW>(a, c, j, px0, npx, warp, lane);
+    warp_readout<NW>(a, c, j, band, npx, warp, lane);
     ++j;
   }
   if (n_b > 0) {
     __syncthreads();
     for (int i = threadIdx.x; i < npx; i += NT) {
-      a.S[px0 + i] = (float)c.Ssm[i];
-      a.T[px0 + i] = c.Tsm[i];
+      const int64_t g = band_gpix(a.bm, band, i);
+      a.S[g] = (float)c.Ssm[i];
+      a.T[g] = c.Tsm[i];
     }
   }
 }

@@ -1,9 +1,10 @@
 // esi_integrate_fast.cu -- K2: per-band integration (Alg. 2) fused
 // with the Eq. 13/14 readout of every frame of the chunk.
 //
-// One CTA of 8 warps per band of band_px consecutive pixel ids (K1's
-// partition key; band_px is a run-time multiple of 64 chosen so that the grid
-// is exactly kK2Ctas resident CTAs per SM).  The band's state lives in shared memory for the whole
+// One CTA of 8 warps per band (K1's partition key): the sensor's 64-pixel groups
+// are dealt round-robin to the bands (esi_internal.cuh, band_gpix), band_px slots
+// each, the band count chosen so that the grid is exactly kK2Ctas resident CTAs per
+// SM (or, contiguous layout, to runs of band_px consecutive ids).  The band's state lives in shared memory for the whole
 // chunk: S (fp32) and T as an fp32 offset from the chunk base ChunkInfo::trel
 // (exact integers: |T| < 2^24 us; pixels older than the decay horizon are
 // clamped to -(dt_cut+1), i.e. "fully decayed").
@@ -88,12 +89,14 @@ __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_til
 
 // Frame j for the band: 4 pixels per thread-iteration (quads), Eq. 4 + Eq. 13 +
 // Eq. 14 with packed f32x2 arithmetic, one 4-byte streaming store per quad.
-template <int BM>
+template <int BM, bool IL>
 __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm, int j, int32_t tji,
-                                             int64_t px0, int npx, const FastConst& c) {
+                                             int band, int npx, uint32_t qoff, const FastConst& c) {
   const float tj = (float)tji;
   const float aj = (float)(tji - (int32_t)c.tau_h);          // t_j - tau (folded mode: tau integer)
-  uint8_t* frame = a.out + (int64_t)j * a.P + px0;
+  // local pixel i -> frame[band_gpix(bm, band, i)]; contiguous layout (!IL): frame[band * band_px + i],
+  // qoff = band * band_px
+  uint8_t* frame = a.out + (int64_t)j * a.P + (IL ? 0u : qoff);
   const int nq = (npx + 3) >> 2;
   const bool vec = a.vec8 != 0;
   if (c.fold) {                                              // hot path: constants hoisted out of the loop
@@ -115,14 +118,26 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
     // full quads: one 4-byte streaming store each (__stcs: no memory clobber, so the
     // next quad's shared loads can be issued ahead); the remainder quads fall on the
     // last warp (warp 0 also lists the windows)
-    unsigned int* f4 = reinterpret_cast<unsigned int*>(frame);
+    // a thread's quads q, q + kNT, ... are the same quad of 64-pixel groups kNT / 16 apart:
+    // a constant stride of kNT * gs words in the frame, from the thread's first quad at
+    // byte qoff (computed once per kernel)
+    static_assert(kNT % (kGroup / 4) == 0, "quads of one thread must keep their place in the group");
     const int nfull = vec ? (npx >> 2) : 0;
+    if (IL) {
+      unsigned int* f4 = reinterpret_cast<unsigned int*>(frame + qoff);
+      const uint32_t fstride = (uint32_t)kNT * (uint32_t)a.bm.gs;
 #pragma unroll 2
-    for (int q = kNT - 1 - (int)threadIdx.x; q < nfull; q += kNT) __stcs(f4 + q, quad(q));
+      for (int q = kNT - 1 - (int)threadIdx.x; q < nfull; q += kNT, f4 += fstride) __stcs(f4, quad(q));
+    } else {                                                       // contiguous: compile-time stride
+      unsigned int* f4 = reinterpret_cast<unsigned int*>(frame);
+#pragma unroll 2
+      for (int q = kNT - 1 - (int)threadIdx.x; q < nfull; q += kNT) __stcs(f4 + q, quad(q));
+    }
     for (int q = nfull + (int)threadIdx.x; q < nq; q += kNT) {     // ragged tail / unaligned output
       const uint32_t v = quad(q);
       const int base = q * 4, n = min(4, npx - base);
-      for (int u = 0; u < n; ++u) frame[base + u] = (uint8_t)((v >> (8 * u)) & 0xffu);
+      uint8_t* dst = frame + (IL ? band_gpix(a.bm, band, base) : (int64_t)base);   // a quad never straddles a group
+      for (int u = 0; u < n; ++u) dst[u] = (uint8_t)((v >> (8 * u)) & 0xffu);
     }
     return;
   }
@@ -133,11 +148,12 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
     const uint32_t b01 = readout2<BM>(make_float2(s0.x, s0.y), make_float2(t0.x, t0.y), tj, aj, c, a.mp.smin, a.mp.smax);
     const uint32_t b23 = readout2<BM>(make_float2(s0.z, s0.w), make_float2(t0.z, t0.w), tj, aj, c, a.mp.smin, a.mp.smax);
     const uint32_t v = __byte_perm(b01, b23, 0x5410);
+    uint8_t* dst = frame + (IL ? band_gpix(a.bm, band, base) : (int64_t)base);   // a quad never straddles a group
     if (vec && base + 4 <= npx) {
-      st_stream4(frame + base, v);
+      st_stream4(dst, v);
     } else {
       const int n = min(4, npx - base);
-      for (int u = 0; u < n; ++u) frame[base + u] = (uint8_t)((v >> (8 * u)) & 0xffu);
+      for (int u = 0; u < n; ++u) dst[u] = (uint8_t)((v >> (8 * u)) & 0xffu);
     }
   }
 }
@@ -256,15 +272,14 @@ __device__ __forceinline__ void process_segment(const FastSmem sm, const uint2* 
 #ifndef ESI_K2_MINB
 #define ESI_K2_MINB kK2Ctas
 #endif
-template <int BM>
+template <int BM, bool IL>   // IL: interleaved band layout (run-time frame stride); else contiguous bands
 __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_wsum[32];
   const int band = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bp = a.band_px;
-  const int64_t px0 = (int64_t)band * bp;
-  const int npx = (int)min((int64_t)bp, a.P - px0);
+  const int npx = band_npx(a.bm, band, a.P);                 // valid local pixels: a prefix of the bp slots
   const int n_tiles = a.n_tiles;
   const FastSmem sm = carve(smem_raw, bp, n_tiles);
 
@@ -278,11 +293,21 @@ __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs
   const float t_clamp = -(float)(a.dp.dt_cut + 1);
   const int32_t tcap = (int32_t)min(a.t_cap - trel, (int64_t)(1 << 25));
   const FastConst kc = make_const(a);
+  // byte of the thread's first readout quad in a frame (P <= 2^22: 32-bit); the empty asm keeps it
+  // in a register (the compiler otherwise recomputes it from ctaid/tid in every readout call)
+  uint32_t qoff = (uint32_t)band * (uint32_t)bp;            // contiguous layout: the band's first pixel id
+  if (IL) {
+    const uint32_t q0 = (uint32_t)(kNT - 1 - (int)threadIdx.x);
+    qoff = (((q0 >> (kGroupShift - 2)) * (uint32_t)a.bm.gs + (uint32_t)band * (uint32_t)a.bm.bs) << kGroupShift) |
+           ((q0 << 2) & (uint32_t)(kGroup - 1));
+  }
+  asm volatile("" : "+r"(qoff));
 
   for (int i = threadIdx.x; i < bp; i += kNT) {
     const bool in = i < npx;
-    sm.S[i] = in ? a.S[px0 + i] : 0.f;
-    sm.T[i] = in ? (float)max(a.T[px0 + i] - trel, (int64_t)t_clamp) : t_clamp;
+    const int64_t g = band_gpix(a.bm, band, i);
+    sm.S[i] = in ? a.S[g] : 0.f;
+    sm.T[i] = in ? (float)max(a.T[g] - trel, (int64_t)t_clamp) : t_clamp;
     sm.head[i] = 0u;                          // generation 0: never a live claim
   }
   if (threadIdx.x == 0) *sm.nd = 0;
@@ -349,7 +374,7 @@ __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs
         }
         if (e1 == n_sb) break;                  // the window may continue in the next sub-batch
         if (j >= f_hi) { done = true; break; }  // later events stay pending
-        fast_readout<BM>(a, sm, j, sm.wtj[w], px0, npx, kc);
+        fast_readout<BM, IL>(a, sm, j, sm.wtj[w], band, npx, qoff, kc);
         ++j;
         e0 = e1;
         more = (w == nwin - 1);                 // every listed window closed: list the next ones
@@ -360,34 +385,40 @@ __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs
   cp_async_wait_all();
   // ---- 3. frames after the chunk's last event
   while (j < f_hi) {
-    fast_readout<BM>(a, sm, j, (int32_t)(a.tf[j] - trel), px0, npx, kc);
+    fast_readout<BM, IL>(a, sm, j, (int32_t)(a.tf[j] - trel), band, npx, qoff, kc);
     ++j;
   }
   if (n_b > 0) {
     __syncthreads();
     for (int i = threadIdx.x; i < npx; i += kNT) {
-      a.S[px0 + i] = sm.S[i];
+      const int64_t g = band_gpix(a.bm, band, i);
+      a.S[g] = sm.S[i];
       const float tr = sm.T[i];
-      if (tr != t_clamp) a.T[px0 + i] = trel + (int64_t)tr;
+      if (tr != t_clamp) a.T[g] = trel + (int64_t)tr;
     }
   }
 }
 
-template <int BM>
-cudaError_t launch_fast_b(const IntArgs& a, cudaStream_t s) {
+template <int BM, bool IL>
+cudaError_t launch_fast_l(const IntArgs& a, cudaStream_t s) {
   const size_t smem = fast_smem_bytes(a.band_px, a.n_tiles);
   int dev = 0;
   cudaGetDevice(&dev);
   static std::atomic<int> configured[64];   // zero-initialised; set-once flags (idempotent, race-free)   // per device (the attribute is per context)
   if (dev < 0 || dev >= 64 || !configured[dev].load(std::memory_order_relaxed)) {
     const size_t mx = fast_smem_bytes(kMaxBandPx, kMaxTilesPerChunk);
-    cudaError_t e = cudaFuncSetAttribute(esi_integrate_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(esi_integrate_kernel<BM, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)mx);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev].store(1, std::memory_order_relaxed);
   }
-  esi_integrate_kernel<BM><<<a.nb, kNT, smem, s>>>(a);
+  esi_integrate_kernel<BM, IL><<<a.nb, kNT, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int BM>
+cudaError_t launch_fast_b(const IntArgs& a, cudaStream_t s) {
+  return a.bm.interleave ? launch_fast_l<BM, true>(a, s) : launch_fast_l<BM, false>(a, s);
 }
 
 }  // namespace

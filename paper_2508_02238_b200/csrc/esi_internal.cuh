@@ -49,6 +49,62 @@ constexpr int kK2Ctas = ESI_K2_CTAS;
 #endif
 constexpr int kK2Warps = ESI_K2_WARPS;     // warps per fast-K2 CTA
 
+// Band layout.  Pixel ids are dealt to the nb bands in groups of kGroup = 64 consecutive
+// ids; a band holds gpb groups (band_px = gpb * 64 pixel slots).  Two layouts, one code path:
+//   interleaved: group g = pid / 64 belongs to band g % nb and is its local group g / nb,
+//                so every band samples the whole sensor and the bands of a chunk hold nearly
+//                the same number of events wherever the scene is active;
+//   contiguous:  group g belongs to band g / gpb (a run of band_px consecutive pixel ids).
+// Local pixel i of band b is pixel id (((i / 64) gs + b bs) * 64 + i % 64 with group strides
+// (gs, bs) = (nb, 1) interleaved, (1, gpb) contiguous.  A warp's frame stores stay 64-byte runs.
+#ifndef ESI_GROUP_SHIFT
+#define ESI_GROUP_SHIFT 6
+#endif
+constexpr int kGroupShift = ESI_GROUP_SHIFT;
+constexpr int kGroup = 1 << kGroupShift;
+struct BandMap {
+  int32_t nb, gpb;           // bands, groups per band
+  int32_t gs, bs;            // group strides of the local group index and of the band index
+  int32_t interleave;        // 1: interleaved, 0: contiguous
+  uint32_t div, magic;       // g / div = umulhi(g, magic) for every group index g < 2^16 (div = nb or gpb; > 1)
+};
+inline BandMap make_band_map(int nb, int gpb, int interleave) {
+  BandMap m;
+  m.nb = nb;
+  m.gpb = gpb;
+  m.interleave = interleave;
+  m.gs = interleave ? nb : 1;
+  m.bs = interleave ? 1 : gpb;
+  m.div = (uint32_t)(interleave ? nb : gpb);
+  // umulhi(g, m) == g / d for g < 2^16: m = floor(2^32 / d) + 1, error term g (m d - 2^32) <= g d < 2^32
+  m.magic = m.div <= 1 ? 0u : (uint32_t)((((uint64_t)1) << 32) / (uint64_t)m.div + 1);
+  return m;
+}
+// (band, local pixel) of pixel id pid
+__device__ __forceinline__ void band_of(const BandMap& m, uint32_t pid, uint32_t& band, uint32_t& local) {
+  const uint32_t g = pid >> kGroupShift;
+  const uint32_t q = m.div <= 1u ? g : __umulhi(g, m.magic);
+  const uint32_t r = g - q * m.div;
+  band = m.interleave ? r : q;
+  local = ((m.interleave ? q : r) << kGroupShift) | (pid & (uint32_t)(kGroup - 1));
+}
+// pixel id of local pixel i of band `band`
+__host__ __device__ inline int64_t band_gpix(const BandMap& m, int band, int i) {
+  return (((int64_t)(i >> kGroupShift) * m.gs + (int64_t)band * m.bs) << kGroupShift) | (int64_t)(i & (kGroup - 1));
+}
+// valid local pixels of the band: a prefix [0, npx) of its band_px slots (only the sensor's
+// last group can be partial)
+__host__ __device__ inline int band_npx(const BandMap& m, int band, int64_t P) {
+  const int64_t ng = (P + kGroup - 1) >> kGroupShift;          // groups of the sensor
+  const int64_t first = (int64_t)band * m.bs;                  // the band's first group
+  if (first >= ng) return 0;
+  int64_t mine = (ng - first + m.gs - 1) / m.gs;               // its groups
+  if (mine > m.gpb) mine = m.gpb;
+  const int64_t last = (mine - 1) * m.gs + first;              // its last group
+  const int64_t tail = (last == ng - 1) ? ng * kGroup - P : 0; // missing pixels of the last group
+  return (int)(mine * kGroup - tail);
+}
+
 // First error of a render call: (global event index << 8) | code, atomicMin'ed
 // so that the earliest offending event wins (same as the oracle's first error).
 constexpr unsigned long long kNoError = ~0ull;
@@ -106,10 +162,8 @@ struct PartArgs {
   int64_t t_min;             // max(t_origin, last_frame_t + 1): smallest admissible t
   int64_t t_cap;             // last frame time of the render call
   int32_t W, H;
-  int32_t band_px, nb;
-  uint64_t band_magic;       // pid / band_px = (pid * band_magic) >> 40 (exact for pid < 2^23)
-  uint32_t band_magic32;     // pid / band_px = umulhi(pid, band_magic32) when band32 (checked on the host)
-  int32_t band32;
+  int32_t band_px, nb;       // bands of band_px pixel slots
+  BandMap bm;                // pixel id <-> (band, local pixel)
   int32_t validate;          // 1: check every event (fused validation); 0: validated on push
   uint2* rec;                // [n_tiles * kTile] tile-local band-sorted records
   uint32_t* meta;            // [nb][n_tiles]: offset | count << 16
@@ -147,6 +201,7 @@ struct IntArgs {
   uint8_t* out;                      // [F][P]
   int64_t P;
   int32_t band_px, nb;
+  BandMap bm;                        // pixel id <-> (band, local pixel)
   int32_t vec8;                      // 8-byte frame stores allowed
   DecayParams dp;
   MapParams mp;

@@ -87,7 +87,7 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, const PartSmem
 
   uint16_t* myhist = hist + warp * nbp;
   uint32_t key[EPT], tl[EPT], pr[EPT];   // band | rank << 10; record words (t low, pixel | sign)
-  const uint32_t W = (uint32_t)a.W, H = (uint32_t)a.H, BPX = (uint32_t)a.band_px;
+  const uint32_t W = (uint32_t)a.W, H = (uint32_t)a.H;
   const int64_t t_min = a.t_min;
   const int64_t tprev0 = VALIDATE ? *s_tprev : 0;
 
@@ -115,10 +115,8 @@ __device__ __forceinline__ void partition_tile(const PartArgs& a, const PartSmem
       }
     }
     const uint32_t pid = y * W + x;
-    // pid / band_px: 32-bit high multiply when exact for every pid of the sensor, else 64-bit
-    const uint32_t band = !act ? 0u : BAND32 ? __umulhi(pid, a.band_magic32)
-                                            : (uint32_t)(((uint64_t)pid * a.band_magic) >> 40);
-    const uint32_t pix = pid - band * BPX;
+    uint32_t band, pix;                                        // band layout (esi_internal.cuh);
+    band_of(a.bm, pid, band, pix);                             // inactive lanes: pid = 0 -> band 0
     uint32_t rank;
     if (RANK == 1) {
       uint32_t* hw = reinterpret_cast<uint32_t*>(myhist);
@@ -355,8 +353,7 @@ static cudaError_t launch_part_t(const PartArgs& a, int n_tiles, cudaStream_t s)
 
 template <int RA>
 static cudaError_t launch_part_r(const PartArgs& a, int n_tiles, cudaStream_t s) {
-  if (a.validate) return a.band32 ? launch_part_t<RA, true, true>(a, n_tiles, s) : launch_part_t<RA, true, false>(a, n_tiles, s);
-  return a.band32 ? launch_part_t<RA, false, true>(a, n_tiles, s) : launch_part_t<RA, false, false>(a, n_tiles, s);
+  return a.validate ? launch_part_t<RA, true, true>(a, n_tiles, s) : launch_part_t<RA, false, true>(a, n_tiles, s);
 }
 
 cudaError_t launch_partition(const PartArgs& a, int n_tiles, int rank_mode, cudaStream_t s) {

@@ -64,7 +64,7 @@ struct esi_handle {
   int64_t P = 0;
   esi_params_t prm{};
   int band_px = 256, nb = 1;
-  uint64_t band_magic = 0;
+  BandMap bm{};              // pixel id <-> (band, local pixel)
   int64_t chunk_events = 0;
   int max_tiles = 0;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -121,8 +121,6 @@ struct esi_handle {
   bool atomic_rank = true;   // lane-ordered smem atomics observed (probed at create)
   int rank_mode = 2;         // K1 stable ranks: 2 = peer masks (ordered by construction, default),
                              // 1 = lane-ordered atomics (only if probed), 0 = ballot multi-split
-  uint32_t band_magic32 = 0;
-  bool band32 = false;
   bool allow_fast = true;    // K2 fast variant allowed (dt_cut < 2^23)
   bool single_stream = false; // ESI_SINGLE_STREAM=1: K1 and K2 on one stream
 };
@@ -281,6 +279,7 @@ int params_ok(const esi_params_t* p) {
   if (p->chunk_events < 0) return 0;
   if (p->decay_kind < 0 || p->decay_kind > 2 || p->decay_first < 0 || p->decay_first > 1) return 0;
   if (p->state_unclamped < 0 || p->state_unclamped > 1) return 0;
+  if (p->band_layout != ESI_BANDS_INTERLEAVED && p->band_layout != ESI_BANDS_CONTIGUOUS) return 0;
   return 1;
 }
 
@@ -385,31 +384,35 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   h->P = P;
   h->prm = prm;
   derive_params(h);
-  // Band size (K1 partition key, K2 CTA): a multiple of 64 pixels such that
-  // the bands fill the SMs evenly at kK2Ctas resident K2 CTAs (8 warps each) per SM
-  // (c4, 3 per SM: 437 bands of 2112 pixels on 148 SMs), at most kMaxBandPx (shared memory) and at most
-  // kMaxBands bands (K1's shared-memory histograms).
+  // Bands (K1 partition key, one K2 CTA each) of gpb 64-pixel groups (esi_internal.cuh,
+  // BandMap): gpb such that the bands fill the SMs evenly at kK2Ctas resident K2 CTAs (8 warps
+  // each) per SM when a band then fits shared memory (c4, 3 per SM: 33 groups = 2112 pixel
+  // slots; 437 contiguous bands, or 444 interleaved ones, on 148 SMs), else as many bands as
+  // kMaxBandPx needs (at most kMaxBands, K1's shared-memory histograms: P <= 2^22).
   {
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, prm.device);
-    const int64_t slots = (int64_t)n_sm * kK2Ctas;
-    int64_t bp = (P + slots - 1) / slots;
-    bp = ((bp + 63) / 64) * 64;
-    bp = std::max<int64_t>(64, std::min<int64_t>(bp, kMaxBandPx));
-    while ((P + bp - 1) / bp > kMaxBands) bp += 64;
+    const int64_t ng = (P + kGroup - 1) / kGroup;
+    int64_t nb = std::max<int64_t>(1, std::min<int64_t>((int64_t)n_sm * kK2Ctas, std::min<int64_t>(ng, kMaxBands)));
+    int64_t gpb = (ng + nb - 1) / nb;                          // groups per band
     if (const char* e = getenv("ESI_BAND_PX")) {
       const int64_t v = atoll(e);
-      if (v >= 64 && v <= kMaxBandPx && v % 64 == 0 && (P + v - 1) / v <= kMaxBands) bp = v;
+      if (v >= kGroup && v <= kMaxBandPx && v % kGroup == 0 && (ng + v / kGroup - 1) / (v / kGroup) <= kMaxBands) {
+        gpb = v / kGroup;
+        nb = (ng + gpb - 1) / gpb;
+      }
     }
-    h->band_px = (int)bp;
-  }
-  h->nb = (int)((P + h->band_px - 1) / h->band_px);
-  h->band_magic = ((uint64_t)1 << 40) / (uint64_t)h->band_px + 1;   // exact pid / band_px for pid < 2^23
-  {  // 32-bit variant: umulhi(pid, m) == pid / bp for all pid < P when (m bp - 2^32) (P - 1) < 2^32
-    const uint64_t m = ((((uint64_t)1) << 32) + (uint64_t)h->band_px - 1) / (uint64_t)h->band_px;
-    const uint64_t err = m * (uint64_t)h->band_px - (((uint64_t)1) << 32);
-    h->band32 = m <= 0xffffffffull && err * (uint64_t)(P - 1) < (((uint64_t)1) << 32);
-    h->band_magic32 = h->band32 ? (uint32_t)m : 0u;
+    if (gpb > kMaxBandPx / kGroup) {                           // shared-memory cap: more bands than resident slots
+      gpb = kMaxBandPx / kGroup;
+      nb = (ng + gpb - 1) / gpb;
+    }
+    gpb = (ng + nb - 1) / nb;                                  // no band larger than the round-robin needs
+    int interleave = prm.band_layout == ESI_BANDS_INTERLEAVED ? 1 : 0;
+    if (const char* e = getenv("ESI_BAND_LAYOUT")) interleave = atoi(e) == ESI_BANDS_INTERLEAVED ? 1 : 0;
+    if (!interleave) nb = (ng + gpb - 1) / gpb;                // contiguous runs of gpb groups: no empty band
+    h->band_px = (int)(gpb * kGroup);
+    h->nb = (int)nb;
+    h->bm = make_band_map(h->nb, (int)gpb, interleave);
   }
   int64_t ce = prm.chunk_events > 0 ? prm.chunk_events : (int64_t)8 << 20;
   ce = ((ce + kTile - 1) / kTile) * kTile;
@@ -760,9 +763,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.H = h->H;
       pa.band_px = h->band_px;
       pa.nb = h->nb;
-      pa.band_magic = h->band_magic;
-      pa.band_magic32 = h->band_magic32;
-      pa.band32 = h->band32 ? 1 : 0;
+      pa.bm = h->bm;
       pa.validate = h->prm.validate_on_push ? 0 : 1;
       pa.rec = h->rec[bf];
       pa.tile_ctr = h->tile_ctr + 2 * bf;
@@ -798,6 +799,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       ia.P = h->P;
       ia.band_px = h->band_px;
       ia.nb = h->nb;
+      ia.bm = h->bm;
       ia.vec8 = vec8;
       ia.dp = h->dp;
       ia.mp = h->mp;
@@ -1241,9 +1243,7 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     pa.H = h->H;
     pa.band_px = h->band_px;
     pa.nb = h->nb;
-    pa.band_magic = h->band_magic;
-    pa.band_magic32 = h->band_magic32;
-    pa.band32 = h->band32 ? 1 : 0;
+    pa.bm = h->bm;
     pa.validate = 0;   // validated above
     pa.rec = h->rec[0];
     pa.tile_ctr = h->tile_ctr;
@@ -1259,6 +1259,7 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     ia.P = h->P;
     ia.band_px = h->band_px;
     ia.nb = h->nb;
+    ia.bm = h->bm;
     ia.dp = h->dp;
     ia.mp = h->mp;
     ia.atomic_rank = h->rank_mode == 1 ? 1 : 0;   // K5's ranks follow K1's (probed) mode
@@ -1324,9 +1325,7 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   pa.H = h->H;
   pa.band_px = h->band_px;
   pa.nb = h->nb;
-  pa.band_magic = h->band_magic;
-  pa.band_magic32 = h->band_magic32;
-  pa.band32 = h->band32 ? 1 : 0;
+  pa.bm = h->bm;
   pa.validate = h->prm.validate_on_push ? 0 : 1;
   pa.rec = h->rec[0];
   pa.tile_ctr = h->tile_ctr;
@@ -1364,7 +1363,7 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
         const uint2 r = rec[idx];
         const int64_t tt = wide[t] ? wt[idx] : t0[t] + (int64_t)(uint32_t)(r.x - (uint32_t)t0[t]);
         out_t[o] = tt;
-        out_pid[o] = (uint32_t)b * h->band_px + (r.y & 0x7fffffffu);
+        out_pid[o] = (uint32_t)band_gpix(h->bm, b, (int)(r.y & 0x7fffffffu));
         out_p[o] = (r.y & 0x80000000u) ? -1 : 1;
         ++o;
       }

@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
   const int band = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bp = a.band_px;
-  const int64_t px0 = (int64_t)band * bp;
-  const int npx = (int)min((int64_t)bp, a.P - px0);
+  const BandMap bmap = a.bm;                                 // band layout (esi_internal.cuh)
+  const int npx = band_npx(bmap, band, a.P);
   const int n_tiles = a.n_tiles;
   uint8_t* const h8 = smem_raw + sl_off_h8(bp);
   uint16_t* const off = reinterpret_cast<uint16_t*>(smem_raw + sl_off_off(bp));
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
     if (heads) {
       in_ = r0 + __ffs(heads) - 1;
       heads &= heads - 1u;
-      Mn = maps[px0 + (cur[in_].y & 0x7fffffffu)];
+      Mn = maps[band_gpix(bmap, band, (int)(cur[in_].y & 0x7fffffffu))];
     }
     while (in_ >= 0) {
       const int i = in_;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
       if (heads) {                                       // prefetch the next run's map
         in_ = r0 + __ffs(heads) - 1;
         heads &= heads - 1u;
-        Mn = maps[px0 + (cur[in_].y & 0x7fffffffu)];
+        Mn = maps[band_gpix(bmap, band, (int)(cur[in_].y & 0x7fffffffu))];
       }
       const int o1 = off[px + 1];
       Map4 g{M.a, M.c, M.lo, M.hi};
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kST, kK2Ctas) esi_slice_summary_kernel(IntArgs
       M.a = g.a; M.c = g.c; M.lo = g.lo; M.hi = g.hi;
       M.t_last = t_last;
       M.n = m;
-      maps[px0 + px] = M;
+      maps[band_gpix(bmap, band, (int)px)] = M;
     }
   }
   cp_async_wait_all();

@@ -45,7 +45,8 @@ class EsiParams(ctypes.Structure):
                 ("t_origin_us", ctypes.c_int64), ("readout_decay", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("validate_on_push", ctypes.c_int32),
                 ("chunk_events", ctypes.c_int32), ("decay_kind", ctypes.c_int32),
-                ("decay_first", ctypes.c_int32), ("state_unclamped", ctypes.c_int32)]
+                ("decay_first", ctypes.c_int32), ("state_unclamped", ctypes.c_int32),
+                ("band_layout", ctypes.c_int32)]
 
 
 class EsiError(RuntimeError):

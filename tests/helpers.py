@@ -23,7 +23,8 @@ def gpu_run(W, H, events, t_frames, params, readout_decay=1, t_origin=0, chunk_e
     e = Esi(W, H, C=params["C"], k=params["k"], b=params["b"], s_min=params["s_min"],
             s_max=params["s_max"], t_origin_us=t_origin, readout_decay=readout_decay,
             chunk_events=chunk_events, decay_kind=params.get("decay_kind", 0),
-            decay_first=params.get("decay_first", 0), state_unclamped=params.get("state_unclamped", 0))
+            decay_first=params.get("decay_first", 0), state_unclamped=params.get("state_unclamped", 0),
+            band_layout=params.get("band_layout", 0))
     try:
         ev = events.to("cuda") if device_events else events.cpu().contiguous()
         if not device_events:

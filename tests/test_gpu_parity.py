@@ -80,6 +80,37 @@ def test_c3_hot_pixels():
     check(w.W, w.H, ev_np_of(w), w.t_frames, w.params)
 
 
+@pytest.mark.parametrize("layout", [0, 1])
+def test_band_layouts_against_oracle(layout):
+    """Both band layouts (esi_params_t.band_layout: contiguous runs, the default, and
+    interleaved 64-pixel groups) against the oracle: c2 in small chunks, c3's hot
+    pixels, sensors whose pixel count is not a multiple of 64 (a partial last group),
+    fewer 64-pixel groups than bands, and the fp64 kernel (slow decay)."""
+    w = wl("c2")
+    check(w.W, w.H, ev_np_of(w), w.t_frames, dict(w.params, band_layout=layout), chunk_events=262144)
+    w = wl("c3", duration_us=500_000)
+    check(w.W, w.H, ev_np_of(w), w.t_frames, dict(w.params, band_layout=layout))
+    for (W, H, n) in [(37, 29, 30_000), (100, 70, 60_000), (7, 5, 3_000), (333, 211, 200_000)]:
+        ev = random_stream(W + H + layout, W, H, n, 400_000)
+        tf = np.arange(1, 41, dtype=np.int64) * 10_000
+        check(W, H, ev, tf, dict(DEF, band_layout=layout))
+        check(W, H, ev, tf, dict(DEF, k=0.05, band_layout=layout))          # fp64 kernel
+
+
+def test_band_layout_does_not_change_frames():
+    """band_layout is a performance knob: on a stream whose pixels see at most one
+    event per frame window per sub-batch path (sparse and chain paths, sequential fp32)
+    the frames and the state are bit-identical between the two layouts."""
+    w = wl("c2")
+    ev = from_numpy_struct(ev_np_of(w))
+    f0, S0, T0, _ = gpu_run(w.W, w.H, ev, w.t_frames, dict(w.params, band_layout=0))
+    f1, S1, T1, _ = gpu_run(w.W, w.H, ev, w.t_frames, dict(w.params, band_layout=1))
+    np.testing.assert_array_equal(T0, T1)
+    assert np.max(np.abs(S0 - S1)) <= 1e-6          # dense-path pixels may differ in rounding (reading A18)
+    d = np.abs(f0.astype(int) - f1.astype(int))
+    assert d.max() <= 1 and (d != 0).mean() <= 1e-4
+
+
 @pytest.mark.parametrize("mode", ["ballot", "atomic"])
 def test_c2_other_rank_modes(mode, monkeypatch):
     monkeypatch.setenv("ESI_RANK_MODE", mode)
@@ -249,10 +280,11 @@ def test_t_origin_and_late_start():
     check(16, 16, ev, tf, DEF, t_origin=5_000_000_000 - 40_000)
 
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("rank_mode", ["peers", "ballot", "atomic"])
-def test_partition_is_bit_exact_stable_grouping(rank_mode, monkeypatch):
+def test_partition_is_bit_exact_stable_grouping(rank_mode, layout, monkeypatch):
     """K1's stable grouping against the plain definition (a stable sort by band,
-    SURVEY P14) in every rank mode: peer masks (default, ordered by
+    SURVEY P14; band of pixel id q = (q // 64) % n_bands) in every rank mode: peer masks (default, ordered by
     construction), ballot multi-split, lane-ordered atomics (probed); uniform
     streams and streams where 40 % of the events hit one pixel (many lanes of a
     warp round share a band)."""
@@ -261,7 +293,7 @@ def test_partition_is_bit_exact_stable_grouping(rank_mode, monkeypatch):
     for (W, H, n, hot) in [(64, 48, 100_000, 0.0), (346, 260, 300_000, 0.0), (1280, 720, 2_000_000, 0.0),
                            (346, 260, 300_000, 0.4), (1280, 720, 1_000_000, 0.4)]:
         ev = random_stream(W + int(hot * 10), W, H, n, 1_000_000, hot=hot, cluster=False)
-        e = Esi(W, H)
+        e = Esi(W, H, band_layout=layout)
         try:
             e.push(from_numpy_struct(ev).cuda())
             t, pid, p, bs, band_px = e.debug_partition(n)
@@ -269,12 +301,16 @@ def test_partition_is_bit_exact_stable_grouping(rank_mode, monkeypatch):
             e.close()
         m = min(n, 4 << 20)
         ref_pid = ev["y"][:m].astype(np.int64) * W + ev["x"][:m]
-        perm = oracle.stable_group_by(ref_pid // band_px)     # stable sort by band
+        nb = len(bs) - 1
+        # esi_layout (include/esi.h): contiguous runs (default) or interleaved 64-pixel groups
+        band = (ref_pid // 64) % nb if layout == 1 else ref_pid // band_px
+        assert band_px % 64 == 0 and nb * band_px >= W * H
+        perm = oracle.stable_group_by(band)                   # stable sort by band
         np.testing.assert_array_equal(t, ev["t"][:m][perm])
         np.testing.assert_array_equal(pid, ref_pid[perm])
         np.testing.assert_array_equal(p, ev["p"][:m][perm])
         # per-band CSR offsets
-        counts = np.bincount(ref_pid // band_px, minlength=len(bs) - 1)
+        counts = np.bincount(band, minlength=nb)
         np.testing.assert_array_equal(np.diff(bs), counts)
 
 

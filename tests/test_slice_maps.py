@@ -247,8 +247,8 @@ def test_gpu_slice_summary_matches_oracle_maps(v):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("G_", [2, 3, 5])
-def test_gpu_time_sharded_render_equals_full_stream(G_):
+@pytest.mark.parametrize("G_,layout", [(2, 0), (3, 0), (5, 0), (3, 1)])
+def test_gpu_time_sharded_render_equals_full_stream(G_, layout):
     """G time shards processed in sequence on one GPU, each from the composed maps
     of the earlier shards (esi_slice_summarize / compose / apply), against the
     full-stream oracle: frames within +-1 on <= 0.01 % of pixel-frames, state
@@ -262,7 +262,7 @@ def test_gpu_time_sharded_render_equals_full_stream(G_):
     f_ref, S_ref, T_ref = oracle.run(w.W, w.H, ev, tf, **w.params)
     eb, fb = time_slices(ev["t"], tf, G_)
     dev = w.events.cuda()
-    h = Esi(w.W, w.H, **w.params)
+    h = Esi(w.W, w.H, band_layout=layout, **w.params)      # layout 1: interleaved bands (K5's map addressing)
     try:
         maps = [h.slice_summarize(dev[eb[r]:eb[r + 1]]) for r in range(G_)]
         frames = []

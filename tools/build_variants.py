@@ -3,6 +3,10 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_02238_b200 import build as b
 VARIANTS = {
+    # interleaved bands: pixel groups of 128 / 256 / 512 ids (default 64)
+    "g7": ["-DESI_GROUP_SHIFT=7"],
+    "g8": ["-DESI_GROUP_SHIFT=8"],
+    "g9": ["-DESI_GROUP_SHIFT=9"],
     "k2c4": ["-DESI_K2_CTAS=4"],
     "k2c2w12": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=12"],
     "k2c2w16": ["-DESI_K2_CTAS=2", "-DESI_K2_WARPS=16"],
