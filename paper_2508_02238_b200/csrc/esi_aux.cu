@@ -47,34 +47,59 @@ cudaError_t launch_readout(const ReadoutArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// facts of chunk c: its first event ev[0], last event ev[n - 1], and the first event time of
+// the next chunk (has_next)
+__device__ __forceinline__ ChunkInfo plan_chunk(const esi_event_t* ev, int64_t n, int c, bool has_next, int64_t t_next,
+                                                const int64_t* tf, int F, int64_t t_cap, int allow_fast) {
+  const int64_t t0 = ev[0].t_us;
+  const int64_t t1 = ev[n - 1].t_us;
+  ChunkInfo ci;
+  ci.tbase = t0;
+  ci.f_lo = c == 0 ? 0 : lower_bound_i64(tf, F, t0);
+  ci.f_hi = has_next ? lower_bound_i64(tf, F, t_next) : F;
+  ci.active = t0 <= t_cap;
+  ci.wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
+  int64_t lo = t0, hi = t1;
+  if (ci.f_lo < ci.f_hi) {
+    lo = min(lo, tf[ci.f_lo]);
+    hi = max(hi, tf[ci.f_hi - 1]);
+  }
+  ci.trel = lo;
+  ci.fast = allow_fast && (hi - lo) < ((int64_t)1 << 24);   // fp32-exact relative times
+  ci._pad = 0;
+  return ci;
+}
+
 __global__ void esi_plan_kernel(const esi_event_t* const* chunk_first, const int64_t* chunk_n,
                                 int n_chunks, const int64_t* tf, int F, int64_t t_cap, int allow_fast,
                                 ChunkInfo* info, int32_t* n_active) {
   // chunk c renders the frames j with t_first(c) <= t_j < t_first(c+1) (chunk 0: t_j < t_first(1))
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_chunks; c += gridDim.x * blockDim.x) {
-    const esi_event_t* ev = chunk_first[c];
-    const int64_t t0 = ev[0].t_us;
-    const int64_t t1 = ev[chunk_n[c] - 1].t_us;
-    ChunkInfo ci;
-    ci.tbase = t0;
-    ci.f_lo = c == 0 ? 0 : lower_bound_i64(tf, F, t0);
-    ci.f_hi = c + 1 < n_chunks ? lower_bound_i64(tf, F, chunk_first[c + 1]->t_us) : F;
-    ci.active = t0 <= t_cap;
-    ci.wide = (t1 - t0) > (int64_t)0xFFFFFFFFLL;
-    int64_t lo = t0, hi = t1;
-    if (ci.f_lo < ci.f_hi) {
-      lo = min(lo, tf[ci.f_lo]);
-      hi = max(hi, tf[ci.f_hi - 1]);
-    }
-    ci.trel = lo;
-    ci.fast = allow_fast && (hi - lo) < ((int64_t)1 << 24);   // fp32-exact relative times
-    ci._pad = 0;
+    const bool has_next = c + 1 < n_chunks;
+    const int64_t t_next = has_next ? chunk_first[c + 1]->t_us : 0;
+    const ChunkInfo ci = plan_chunk(chunk_first[c], chunk_n[c], c, has_next, t_next, tf, F, t_cap, allow_fast);
     info[c] = ci;
     // first events are non-decreasing: the active chunks are a prefix
-    const bool next_active = c + 1 < n_chunks && chunk_first[c + 1]->t_us <= t_cap;
+    const bool next_active = has_next && t_next <= t_cap;
     if (ci.active && !next_active) *n_active = c + 1;
     if (c == 0 && !ci.active) *n_active = 0;
   }
+}
+
+// Render of a single chunk whose plan the host does not read back (esi_runtime.cpp, "sync-free"):
+// the chunk's facts from by-value arguments; also resets the render's error word and K1's
+// work counters (instead of two memsets on the stream).
+__global__ void esi_plan1_kernel(const esi_event_t* first, int64_t n, const int64_t* tf, int F, int64_t t_cap,
+                                 int allow_fast, ChunkInfo* info, unsigned long long* err, uint32_t* tile_ctr) {
+  info[0] = plan_chunk(first, n, 0, false, 0, tf, F, t_cap, allow_fast);
+  *err = kNoError;
+  tile_ctr[0] = tile_ctr[1] = tile_ctr[2] = tile_ctr[3] = 0u;
+}
+
+cudaError_t launch_plan1(const esi_event_t* first, int64_t n, const int64_t* tf, int F, int64_t t_cap, int allow_fast,
+                         ChunkInfo* info, unsigned long long* err, uint32_t* tile_ctr, cudaStream_t s) {
+  esi_plan1_kernel<<<1, 1, 0, s>>>(first, n, tf, F, t_cap, allow_fast, info, err, tile_ctr);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_plan(const esi_event_t* const* chunk_first, const int64_t* chunk_n, int n_chunks,
@@ -101,6 +126,27 @@ __global__ void esi_consume_kernel(const esi_event_t* seg, int64_t n, int64_t t_
 cudaError_t launch_consume(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* count,
                            int64_t* last_t, cudaStream_t s) {
   esi_consume_kernel<<<1, 1, 0, s>>>(seg, n, t_cap, count, last_t);
+  return cudaGetLastError();
+}
+
+// consume of the sync-free one-chunk render: res[0] = events consumed, res[1] = the render's
+// error word, res[2] = the plan's kernel choice (one read-back instead of three)
+__global__ void esi_finish1_kernel(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* res, int64_t* last_t,
+                                   const unsigned long long* err, const ChunkInfo* info) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (seg[mid].t_us <= t_cap) lo = mid + 1; else hi = mid;
+  }
+  res[0] = lo;
+  if (lo > 0) *last_t = seg[lo - 1].t_us;
+  res[1] = (int64_t)*err;
+  res[2] = info->fast;
+}
+
+cudaError_t launch_finish1(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* res, int64_t* last_t,
+                           const unsigned long long* err, const ChunkInfo* info, cudaStream_t s) {
+  esi_finish1_kernel<<<1, 1, 0, s>>>(seg, n, t_cap, res, last_t, err, info);
   return cudaGetLastError();
 }
 

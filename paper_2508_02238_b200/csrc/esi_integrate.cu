@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
 
   if (a.gate && *a.gate != kNoError) return;   // lazy validation found an invalid event: write nothing
   const ChunkInfo ci = *a.info;
+  if (a.kind_gate == 2 && ci.fast) return;     // the fast kernel renders this chunk
   const int f_lo = ci.f_lo, f_hi = ci.f_hi;
   const bool active = ci.active != 0;
   if (!active && f_lo >= f_hi) return;

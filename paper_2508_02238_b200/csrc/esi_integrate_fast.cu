@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs
 
   if (a.gate && *a.gate != kNoError) return;   // lazy validation found an invalid event: write nothing
   const ChunkInfo ci = *a.info;
+  if (a.kind_gate == 1 && !ci.fast) return;    // the general kernel renders this chunk
   const int f_lo = ci.f_lo, f_hi = ci.f_hi;
   const bool active = ci.active != 0;
   if (!active && f_lo >= f_hi) return;

@@ -171,6 +171,7 @@ struct PartArgs {
   int32_t* tile_wide;        // [n_tiles]
   int64_t* wide_t;           // [n_tiles * kTile] full t, written for wide tiles only
   unsigned long long* err;
+  const struct ChunkInfo* gate_info;   // non-null: exit at once unless gate_info->active (sync-free single-chunk render)
 };
 
 // Per-chunk facts computed once by esi_plan_kernel (one thread per chunk).
@@ -208,6 +209,9 @@ struct IntArgs {
   WideParams wp;
   const unsigned long long* gate;    // non-null: exit without writing if *gate != kNoError
   int32_t atomic_rank;               // warp-wide shared atomics serve lanes in lane order (probed)
+  // sync-free single-chunk render: the host launches the fast and the general kernel without
+  // reading the plan back; 1: run only if info->fast, 2: only if !info->fast, 0: run
+  int32_t kind_gate;
 };
 
 struct ReadoutArgs {
@@ -238,6 +242,12 @@ cudaError_t launch_readout(const ReadoutArgs& a, cudaStream_t s);
 cudaError_t launch_plan(const esi_event_t* const* chunk_first, const int64_t* chunk_n, int n_chunks,
                         const int64_t* tf, int F, int64_t t_cap, int allow_fast, ChunkInfo* info,
                         int32_t* n_active, cudaStream_t s);
+// sync-free one-chunk render: plan from by-value arguments (+ error word / K1 counter reset), and a
+// consume that packs {consumed, error word, kernel choice} into res[0..2]
+cudaError_t launch_plan1(const esi_event_t* first, int64_t n, const int64_t* tf, int F, int64_t t_cap, int allow_fast,
+                         ChunkInfo* info, unsigned long long* err, uint32_t* tile_ctr, cudaStream_t s);
+cudaError_t launch_finish1(const esi_event_t* seg, int64_t n, int64_t t_cap, int64_t* res, int64_t* last_t,
+                           const unsigned long long* err, const ChunkInfo* info, cudaStream_t s);
 // fast kernel (32-bit relative times, dt_cut < 2^23) -- esi_integrate_fast.cu
 cudaError_t launch_integrate_fast(const IntArgs& a, cudaStream_t s);
 // consume: for segment k, count events with t <= t_cap (binary search), and set

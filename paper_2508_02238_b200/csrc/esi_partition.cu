@@ -273,7 +273,9 @@ __global__ void __launch_bounds__(kPartThreads, kPartCtas) esi_partition_kernel(
   __shared__ __align__(8) uint64_t s_mbar;
   __shared__ int64_t s_tprev;
   __shared__ int s_wide;
-  // (the host launches K1 only for chunks whose first event is <= the render's last frame)
+  // (the host launches K1 only for chunks whose first event is <= the render's last frame; a
+  // sync-free single-chunk render has not read the plan back and leaves that test to the kernel)
+  if (a.gate_info && !a.gate_info->active) return;
   const int nbp = (a.nb + 7) & ~7;
   PartSmem sm;
   sm.raw = reinterpret_cast<int4*>(smem);

@@ -123,6 +123,7 @@ struct esi_handle {
                              // 1 = lane-ordered atomics (only if probed), 0 = ballot multi-split
   bool allow_fast = true;    // K2 fast variant allowed (dt_cut < 2^23)
   bool single_stream = false; // ESI_SINGLE_STREAM=1: K1 and K2 on one stream
+  bool sync_plan = false;     // ESI_SYNC_PLAN=1: read the plan back in every render (no sync-free one-chunk path)
 };
 
 namespace {
@@ -455,6 +456,7 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   // accumulate them in fp64 (wide kernel) rather than fp32
   h->allow_fast = h->dp.dt_cut < ((int64_t)1 << 23) && !h->dp.unclamped && !getenv("ESI_DISABLE_FAST");
   h->single_stream = getenv("ESI_SINGLE_STREAM") && atoi(getenv("ESI_SINGLE_STREAM")) != 0;
+  h->sync_plan = getenv("ESI_SYNC_PLAN") && atoi(getenv("ESI_SYNC_PLAN")) != 0;
   if (!rc) {
     // K1 rank mode: probe that warp-wide smem atomics serve same-address lanes in lane order
     const char* mode = getenv("ESI_RANK_MODE");
@@ -690,30 +692,47 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     rc = ensure_dev(h, &h->d_chunk_first, &h->cf_cap, nc);
     if (!rc) rc = ensure_dev(h, &h->d_chunk_n, &h->cn_cap, nc);
     if (!rc) rc = ensure_dev(h, &h->d_info, &h->info_cap, nc);
-    if (!rc) rc = ensure_pinned(h, nc * 16 + h->segs.size() * sizeof(int64_t) + 128);
+    if (!rc) rc = ensure_pinned(h, nc * 16 + h->segs.size() * sizeof(int64_t) + 128 + sizeof(ChunkInfo));
     if (rc) return rc;
-    const esi_event_t** hcf = (const esi_event_t**)h->h_pin;
-    int64_t* hcn = (int64_t*)(h->h_pin + nc * sizeof(void*));
-    for (size_t c = 0; c < nc; ++c) {
-      hcf[c] = chunks[c].ptr;
-      hcn[c] = chunks[c].n;
-    }
-    ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_first, hcf, nc * sizeof(void*), cudaMemcpyHostToDevice, st));
-    ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_n, hcn, nc * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    h->st_launches += 1;   // plan
-    std::optional<NvtxRange> plan_range;
-    plan_range.emplace("render: plan (+ host read-back)");
-    ESI_CUDA(h, launch_plan(h->d_chunk_first, h->d_chunk_n, (int)nc, h->d_tf, (int)F, t_cap,
-                            h->allow_fast ? 1 : 0, h->d_info, h->d_n_active, st));
+    // A render of one device-resident chunk (the streaming case: one packet, one frame) does
+    // not read the plan back: the chunk is rendered by whichever K2 variant the plan chose --
+    // both are launched and the other one exits at once (IntArgs::kind_gate) -- K1 tests the
+    // chunk's `active` flag itself, and chunk 0 of a one-chunk render owns every frame.  Its
+    // plan takes the chunk by value and resets the error word and K1's counters, K1 runs on
+    // the handle's stream (nothing to overlap with), and one kernel packs the consumed count,
+    // the error word and the plan's choice for a single read-back: one host synchronisation
+    // and about half the stream operations of the general path.
+    const bool nosync = nc == 1 && !chunks[0].host && !h->sync_plan;
     int32_t* hna = (int32_t*)(h->h_pin + nc * 16 + 16);
-    ESI_CUDA(h, cudaMemcpyAsync(hna, h->d_n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     std::vector<ChunkInfo> hinfo(nc);
-    ESI_CUDA(h, cudaMemcpyAsync(hinfo.data(), h->d_info, nc * sizeof(ChunkInfo), cudaMemcpyDeviceToHost, st));
-    ESI_CUDA(h, cudaStreamSynchronize(st));
-    plan_range.reset();
+    h->st_launches += 1;   // plan
+    if (nosync) {
+      ESI_CUDA(h, launch_plan1(chunks[0].ptr, chunks[0].n, h->d_tf, (int)F, t_cap, h->allow_fast ? 1 : 0,
+                               h->d_info, h->d_err, h->tile_ctr, st));
+      *hna = 1;
+      memset(&hinfo[0], 0, sizeof(ChunkInfo));
+      hinfo[0].active = 1;
+      hinfo[0].f_lo = 0;
+      hinfo[0].f_hi = (int32_t)F;
+    } else {
+      const esi_event_t** hcf = (const esi_event_t**)h->h_pin;
+      int64_t* hcn = (int64_t*)(h->h_pin + nc * sizeof(void*));
+      for (size_t c = 0; c < nc; ++c) {
+        hcf[c] = chunks[c].ptr;
+        hcn[c] = chunks[c].n;
+      }
+      ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_first, hcf, nc * sizeof(void*), cudaMemcpyHostToDevice, st));
+      ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_n, hcn, nc * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      NvtxRange plan_range("render: plan (+ host read-back)");
+      ESI_CUDA(h, launch_plan(h->d_chunk_first, h->d_chunk_n, (int)nc, h->d_tf, (int)F, t_cap,
+                              h->allow_fast ? 1 : 0, h->d_info, h->d_n_active, st));
+      ESI_CUDA(h, cudaMemcpyAsync(hna, h->d_n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      ESI_CUDA(h, cudaMemcpyAsync(hinfo.data(), h->d_info, nc * sizeof(ChunkInfo), cudaMemcpyDeviceToHost, st));
+      ESI_CUDA(h, cudaStreamSynchronize(st));
+      ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
+      ESI_CUDA(h, cudaMemsetAsync(h->tile_ctr, 0, 4 * sizeof(uint32_t), st));   // K1 work counters (robust to an aborted launch)
+    }
     const int n_act = std::max(1, *hna);
-    ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
-    ESI_CUDA(h, cudaMemsetAsync(h->tile_ctr, 0, 4 * sizeof(uint32_t), st));   // K1 work counters (robust to an aborted launch)
     const bool lazy = !h->prm.validate_on_push;
     if (lazy) {   // lazy validation (fused in K1): keep the state so that a failing render leaves it untouched
       if (!h->dS_snap) {
@@ -730,7 +749,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     // K1 runs on the aux stream, K2 on the handle's stream; chunk c uses buffer c & 1:
     // K1(c) waits for the render's setup and for K2(c-2); K2(c) waits for K1(c).
     // (ESI_SINGLE_STREAM=1: both kernels on the handle's stream, no cross-stream events)
-    const bool two = !h->single_stream;
+    const bool two = !h->single_stream && !nosync;
     cudaStream_t k1s = two ? h->aux : st;
     if (two) {
       ESI_CUDA(h, cudaEventRecord(h->ev_start, st));
@@ -750,7 +769,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
         ESI_CUDA(h, cudaStreamWaitEvent(k1s, h->ev_h2d[bf], 0));
         k1_ev = h->stage_ev[bf];
       }
-      PartArgs pa;
+      PartArgs pa{};
       pa.ev = k1_ev;
       pa.n = ch.n;
       pa.index_base = index_base;
@@ -772,6 +791,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       pa.tile_wide = h->tile_wide[bf];
       pa.wide_t = h->wide_t[bf];
       pa.err = h->d_err;
+      pa.gate_info = nosync ? h->d_info + c : nullptr;
       if (hinfo[c].active) {   // a chunk entirely after the last frame (only chunk 0 can be) is not partitioned
         TimedLaunch t1;
         timed_begin(h, 0, &t1, k1s);
@@ -782,7 +802,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       if (two || any_host) ESI_CUDA(h, cudaEventRecord(h->ev_k1[bf], k1s));
       if (two) ESI_CUDA(h, cudaStreamWaitEvent(st, h->ev_k1[bf], 0));
 
-      IntArgs ia;
+      IntArgs ia{};
       ia.info = h->d_info + c;
       ia.rec = h->rec[bf];
       ia.meta = h->meta[bf];
@@ -807,7 +827,15 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       ia.gate = lazy ? h->d_err : nullptr;   // a K1 error so far: K2 exits (frames unspecified, S/T restored)
       TimedLaunch t2;
       timed_begin(h, 1, &t2);
-      if (hinfo[c].fast) {
+      if (nosync) {          // the plan decides on the device which of the two runs
+        if (h->allow_fast) {
+          ia.kind_gate = 1;
+          ESI_CUDA(h, launch_integrate_fast(ia, st));
+          h->st_launches += 1;
+        }
+        ia.kind_gate = h->allow_fast ? 2 : 0;
+        ESI_CUDA(h, launch_integrate(ia, st));
+      } else if (hinfo[c].fast) {
         ESI_CUDA(h, launch_integrate_fast(ia, st));
         h->st_fast += 1;
       } else {
@@ -827,17 +855,27 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     }
     // consumed events per segment (segments after the last active chunk consume none)
     const int last_seg = chunks[n_act - 1].seg;
-    rc = ensure_dev(h, &h->d_cons, &h->cons_cap, h->segs.size());
+    rc = ensure_dev(h, &h->d_cons, &h->cons_cap, std::max<size_t>(3, h->segs.size()));
     if (rc) return rc;
-    for (int k = 0; k <= last_seg; ++k) {
-      ESI_CUDA(h, launch_consume(h->segs[k].ptr, h->segs[k].n, t_cap, h->d_cons + k, h->d_last_t, st));
-      h->st_launches += 1;
-    }
     int64_t* hcons = (int64_t*)h->h_pin;
-    unsigned long long* herr = (unsigned long long*)(h->h_pin + (last_seg + 1) * sizeof(int64_t));
-    ESI_CUDA(h, cudaMemcpyAsync(hcons, h->d_cons, (last_seg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    ESI_CUDA(h, cudaMemcpyAsync(herr, h->d_err, sizeof(*herr), cudaMemcpyDeviceToHost, st));
-    ESI_CUDA(h, cudaStreamSynchronize(st));
+    unsigned long long* herr;
+    if (nosync) {   // one segment: {consumed, error word, kernel choice} in one kernel and one read-back
+      ESI_CUDA(h, launch_finish1(h->segs[0].ptr, h->segs[0].n, t_cap, h->d_cons, h->d_last_t, h->d_err, h->d_info, st));
+      h->st_launches += 1;
+      herr = (unsigned long long*)(hcons + 1);
+      ESI_CUDA(h, cudaMemcpyAsync(hcons, h->d_cons, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      ESI_CUDA(h, cudaStreamSynchronize(st));
+      if (hcons[2]) h->st_fast += 1;
+    } else {
+      for (int k = 0; k <= last_seg; ++k) {
+        ESI_CUDA(h, launch_consume(h->segs[k].ptr, h->segs[k].n, t_cap, h->d_cons + k, h->d_last_t, st));
+        h->st_launches += 1;
+      }
+      herr = (unsigned long long*)(h->h_pin + (last_seg + 1) * sizeof(int64_t));
+      ESI_CUDA(h, cudaMemcpyAsync(hcons, h->d_cons, (last_seg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      ESI_CUDA(h, cudaMemcpyAsync(herr, h->d_err, sizeof(*herr), cudaMemcpyDeviceToHost, st));
+      ESI_CUDA(h, cudaStreamSynchronize(st));
+    }
     if (*herr != kNoError) {
       h->sticky = (int)(*herr & 0xff);
       if (lazy) {   // restore the state of the render's start; nothing is consumed
@@ -1230,7 +1268,7 @@ int esi_slice_summarize(esi_handle_t* h, const esi_event_t* events, size_t n, es
     if (t01[2 * c + 1] - t01[2 * c] >= ((int64_t)1 << 31)) { fail(ESI_ERR_INVALID_ARG); break; }
     cudaError_t e = cudaSuccess;
     const int n_tiles = (int)((nc + kTile - 1) / kTile);
-    PartArgs pa;
+    PartArgs pa{};
     pa.ev = ev + o;
     pa.n = nc;
     pa.index_base = o;
@@ -1312,7 +1350,7 @@ int esi_debug_partition(esi_handle_t* h, int64_t* out_t, uint32_t* out_pid, int8
   const int64_t n = std::min(h->chunk_events, s.n);
   if ((int64_t)n_out < n || !out_t || !out_pid || !out_p) return ESI_ERR_INVALID_ARG;
   const int n_tiles = (int)((n + kTile - 1) / kTile);
-  PartArgs pa;
+  PartArgs pa{};
   pa.ev = s.ptr;
   pa.n = n;
   pa.index_base = 0;
