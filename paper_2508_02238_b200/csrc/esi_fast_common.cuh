@@ -16,6 +16,7 @@ struct FastConst {
   float scale, off_frac, magic_off;    // map: byte = low8(bits(rd(v*scale + off_frac + 2^23 + off_int)))
   float scale_w2;                      // k_us^2 * scale: Eq. 14 of S*(k w)^2 with k^2 folded in
   int32_t tau_int;                     // tau is an integer (tau_l == 0)
+  int32_t tau_i;                       // (int32_t)tau_h: tau itself in the folded mode
   int32_t fold;                        // readout mode: 1 = folded (b = 2, readout decay, no clamp, integer tau)
   int32_t rd, cl;                      // readout decay; readout clamp needed (bounds exclude 0)
   float dtc;                           // exponential variant: d = 0 for dt >= dtc (k dt >= 24)
@@ -37,6 +38,7 @@ __device__ __forceinline__ FastConst make_const(const IntArgs& a) {
   c.magic_off = a.mp.magic_off;
   c.scale_w2 = a.mp.scale_w2;
   c.tau_int = a.dp.tau_l == 0.f;
+  c.tau_i = a.dp.tau_i;
   c.rd = a.mp.readout_decay != 0;
   c.cl = a.mp.readout_clamp;           // bounds exclude 0, or unclamped state: clamp at readout
   c.fold = a.dp.bmode == 2 && c.rd && !c.cl && c.tau_int;   // readout only: independent of the order

@@ -91,7 +91,8 @@ __device__ __forceinline__ FastSmem carve(unsigned char* base, int bp, int n_til
 // Eq. 14 with packed f32x2 arithmetic, one 4-byte streaming store per quad.
 template <int BM, bool IL>
 __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm, int j, int32_t tji,
-                                             int band, int npx, uint32_t qoff, const FastConst& c) {
+                                             int band, int npx, uint32_t qoff, const FastConst& c,
+                                             bool tail_only = false) {   // tail_only: fold_readout wrote the full quads
   const float tj = (float)tji;
   const float aj = (float)(tji - (int32_t)c.tau_h);          // t_j - tau (folded mode: tau integer)
   // local pixel i -> frame[band_gpix(bm, band, i)]; contiguous layout (!IL): frame[band * band_px + i],
@@ -123,7 +124,8 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
     // byte qoff (computed once per kernel)
     static_assert(kNT % (kGroup / 4) == 0, "quads of one thread must keep their place in the group");
     const int nfull = vec ? (npx >> 2) : 0;
-    if (IL) {
+    if (tail_only) {
+    } else if (IL) {
       unsigned int* f4 = reinterpret_cast<unsigned int*>(frame + qoff);
       const uint32_t fstride = (uint32_t)kNT * (uint32_t)a.bm.gs;
 #pragma unroll 2
@@ -158,6 +160,63 @@ __device__ __forceinline__ void fast_readout(const IntArgs& a, const FastSmem sm
   }
 }
 
+
+// Per-thread readout state of the folded mode, fixed for the whole chunk and pinned in
+// registers (the compiler otherwise rebuilds the shared-memory bases, the frame pointer and the
+// quad count from ctaid / tid / kernel arguments in every call: ~25 of a call's ~80 instructions).
+struct RoState {
+  uint32_t sS;        // shared address of the thread's first S quad (its T quad: + 4 * band_px)
+  uint8_t* fptr;      // the thread's first quad in the next frame to be written (advances by P)
+  int nmy;            // full quads of this thread (q0, q0 + kNT, ...) | kRagged if the band also has a
+                      // partial last quad or the output is unaligned (byte-store tail, rare)
+};
+constexpr int kRagged = 0x100;
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
+// Frame j of the band in the folded mode (b = 2, readout decay, integer tau, bounds containing
+// 0; fast_readout's hot path): x = S max(T - (t_j - tau), 0)^2 (k^2 scale) + off, Eq. 14 by the
+// round-down magic add.  Two quads per iteration, loads first.  FSTRIDE: bytes between a
+// thread's consecutive quads in the frame (contiguous layout: compile-time 4 * kNT).
+template <bool IL>
+__device__ __forceinline__ void fold_readout(const IntArgs& a, RoState& ro, int32_t tji, uint32_t t_off,
+                                             uint32_t fstride_il, const FastConst& c) {
+  const float najs = -(float)(tji - c.tau_i);                    // -(t_j - tau), exact
+  const float2 naj = make_float2(najs, najs);
+  const float2 sw2 = make_float2(c.scale_w2, c.scale_w2), off = make_float2(c.off_frac, c.off_frac);
+  const float2 mo = make_float2(c.magic_off, c.magic_off);
+  auto quad = [&](const float4 s0, const float4 t0) -> uint32_t {
+    float2 w0 = __fadd2_rn(make_float2(t0.x, t0.y), naj), w1 = __fadd2_rn(make_float2(t0.z, t0.w), naj);
+    w0.x = fmaxf(w0.x, 0.f); w0.y = fmaxf(w0.y, 0.f); w1.x = fmaxf(w1.x, 0.f); w1.y = fmaxf(w1.y, 0.f);
+    const float2 v0 = __fmul2_rn(make_float2(s0.x, s0.y), __fmul2_rn(w0, w0));
+    const float2 v1 = __fmul2_rn(make_float2(s0.z, s0.w), __fmul2_rn(w1, w1));
+    const float2 r0 = __fadd2_rd(__ffma2_rn(v0, sw2, off), mo), r1 = __fadd2_rd(__ffma2_rn(v1, sw2, off), mo);
+    return __byte_perm(__byte_perm(__float_as_uint(r0.x), __float_as_uint(r0.y), 0x0040),
+                       __byte_perm(__float_as_uint(r1.x), __float_as_uint(r1.y), 0x0040), 0x5410);
+  };
+  const uint32_t fstride = IL ? fstride_il : (uint32_t)(4 * kNT);
+  uint32_t sa = ro.sS;
+  uint8_t* f = ro.fptr;
+  int r = 0;
+  const int nmy = ro.nmy & (kRagged - 1);
+  for (; r + 2 <= nmy; r += 2) {
+    const float4 s0 = lds128(sa), t0 = lds128(sa + t_off);
+    const float4 s1 = lds128(sa + kNT * 16), t1 = lds128(sa + t_off + kNT * 16);
+    __stcs(reinterpret_cast<unsigned int*>(f), quad(s0, t0));
+    __stcs(reinterpret_cast<unsigned int*>(f + fstride), quad(s1, t1));
+    sa += 2 * kNT * 16;
+    f += 2 * (size_t)fstride;
+  }
+  if (r < nmy) {
+    const float4 s0 = lds128(sa), t0 = lds128(sa + t_off);
+    __stcs(reinterpret_cast<unsigned int*>(f), quad(s0, t0));
+  }
+  ro.fptr += a.P;
+}
 
 // Per-event processing of one segment (the events of one frame window inside
 // one sub-batch), block-wide.  Each event claims its pixel with an atomic
@@ -294,16 +353,31 @@ __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs
   const float t_clamp = -(float)(a.dp.dt_cut + 1);
   const int32_t tcap = (int32_t)min(a.t_cap - trel, (int64_t)(1 << 25));
   const FastConst kc = make_const(a);
-  // byte of the thread's first readout quad in a frame (P <= 2^22: 32-bit); the empty asm keeps it
-  // in a register (the compiler otherwise recomputes it from ctaid/tid in every readout call)
-  uint32_t qoff = (uint32_t)band * (uint32_t)bp;            // contiguous layout: the band's first pixel id
-  if (IL) {
-    const uint32_t q0 = (uint32_t)(kNT - 1 - (int)threadIdx.x);
+  // byte of the thread's first readout quad in a frame (P <= 2^22: 32-bit); contiguous layout:
+  // the band's first pixel id
+  uint32_t qoff = (uint32_t)band * (uint32_t)bp;
+  const uint32_t q0 = (uint32_t)(kNT - 1 - (int)threadIdx.x);
+  if (IL)
     qoff = (((q0 >> (kGroupShift - 2)) * (uint32_t)a.bm.gs + (uint32_t)band * (uint32_t)a.bm.bs) << kGroupShift) |
            ((q0 << 2) & (uint32_t)(kGroup - 1));
-  }
-  asm volatile("" : "+r"(qoff));
-
+  // folded readout: per-thread state for the whole chunk, pinned in registers by the empty asm
+  RoState ro;
+  const int nfull = a.vec8 ? (npx >> 2) : 0;
+  const bool ragged = nfull != ((npx + 3) >> 2);              // partial last quad, or an unaligned output
+  ro.nmy = (nfull > (int)q0 ? (nfull - (int)q0 + kNT - 1) / kNT : 0) | (ragged ? kRagged : 0);
+  ro.sS = (uint32_t)__cvta_generic_to_shared(sm.S) + q0 * 16u;
+  ro.fptr = a.out + (int64_t)f_lo * a.P + (IL ? qoff : qoff + q0 * 4u);
+  asm volatile("" : "+r"(ro.sS), "+l"(ro.fptr), "+r"(ro.nmy));
+  const uint32_t t_off = (uint32_t)bp * 4u;                   // T follows S in shared memory (carve)
+  const uint32_t fstride_il = 4u * (uint32_t)kNT * (uint32_t)a.bm.gs;
+  auto readout = [&](int jj, int32_t tji) {
+    if (kc.fold) {
+      fold_readout<IL>(a, ro, tji, t_off, fstride_il, kc);
+      if (ro.nmy >= kRagged) fast_readout<BM, IL>(a, sm, jj, tji, band, npx, qoff, kc, true);
+    } else {
+      fast_readout<BM, IL>(a, sm, jj, tji, band, npx, qoff, kc);
+    }
+  };
   for (int i = threadIdx.x; i < bp; i += kNT) {
     const bool in = i < npx;
     const int64_t g = band_gpix(a.bm, band, i);
@@ -375,7 +449,7 @@ __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs
         }
         if (e1 == n_sb) break;                  // the window may continue in the next sub-batch
         if (j >= f_hi) { done = true; break; }  // later events stay pending
-        fast_readout<BM, IL>(a, sm, j, sm.wtj[w], band, npx, qoff, kc);
+        readout(j, sm.wtj[w]);
         ++j;
         e0 = e1;
         more = (w == nwin - 1);                 // every listed window closed: list the next ones
@@ -386,7 +460,7 @@ __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs
   cp_async_wait_all();
   // ---- 3. frames after the chunk's last event
   while (j < f_hi) {
-    fast_readout<BM, IL>(a, sm, j, (int32_t)(a.tf[j] - trel), band, npx, qoff, kc);
+    readout(j, (int32_t)(a.tf[j] - trel));
     ++j;
   }
   if (n_b > 0) {

@@ -124,6 +124,7 @@ struct DecayParams {
   float b;
   // fast K2: u = kf * ((tau_h - dt) + tau_l) with tau = 1e6/k us = tau_h + tau_l
   float tau_h, tau_l, kf;
+  int32_t tau_i;         // (int32_t)tau_h (the fast K2's folded readout: tau is an integer there)
 };
 
 struct MapParams {

@@ -296,6 +296,7 @@ void derive_params(esi_handle_t* h) {
   h->dp.use_f64 = h->dp.dt_cut > (int64_t)(1 << 24);
   h->dp.b = (float)p.b;
   h->dp.tau_h = (float)horizon;
+  h->dp.tau_i = h->dp.tau_h < 2.0e9f ? (int32_t)h->dp.tau_h : 0;   // used by the fast K2 only (tau < 2^23 there)
   h->dp.tau_l = (float)(horizon - (double)h->dp.tau_h);
   h->dp.kf = (float)kk;
   h->dp.bmode = p.decay_kind == 2 ? kDecayNone
