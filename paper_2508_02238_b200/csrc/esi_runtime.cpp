@@ -704,6 +704,33 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     // the error word and the plan's choice for a single read-back: one host synchronisation
     // and about half the stream operations of the general path.
     const bool nosync = nc == 1 && !chunks[0].host && !h->sync_plan;
+    auto k1_args = [&](int c, const esi_event_t* k1_ev, int64_t index_base) {
+      const int bf = c & 1;
+      PartArgs pa{};
+      pa.ev = k1_ev;
+      pa.n = chunks[c].n;
+      pa.index_base = index_base;
+      pa.prev_t = (c == 0) ? h->d_last_t : &chunks[c - 1].ptr[chunks[c - 1].n - 1].t_us;
+      pa.t_origin = h->prm.t_origin_us;
+      pa.last_frame_t = h->has_last_frame ? h->last_frame_t : INT64_MIN;
+      pa.t_min = h->has_last_frame ? std::max(h->prm.t_origin_us, h->last_frame_t + 1) : h->prm.t_origin_us;
+      pa.t_cap = t_cap;
+      pa.W = h->W;
+      pa.H = h->H;
+      pa.band_px = h->band_px;
+      pa.nb = h->nb;
+      pa.bm = h->bm;
+      pa.validate = h->prm.validate_on_push ? 0 : 1;
+      pa.rec = h->rec[bf];
+      pa.tile_ctr = h->tile_ctr + 2 * bf;
+      pa.meta = h->meta[bf];
+      pa.tile_t0 = h->tile_t0[bf];
+      pa.tile_wide = h->tile_wide[bf];
+      pa.wide_t = h->wide_t[bf];
+      pa.err = h->d_err;
+      pa.gate_info = nullptr;
+      return pa;
+    };
     int32_t* hna = (int32_t*)(h->h_pin + nc * 16 + 16);
     std::vector<ChunkInfo> hinfo(nc);
     h->st_launches += 1;   // plan
@@ -724,14 +751,14 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       }
       ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_first, hcf, nc * sizeof(void*), cudaMemcpyHostToDevice, st));
       ESI_CUDA(h, cudaMemcpyAsync(h->d_chunk_n, hcn, nc * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
+      ESI_CUDA(h, cudaMemsetAsync(h->tile_ctr, 0, 4 * sizeof(uint32_t), st));   // K1 work counters (robust to an aborted launch)
       NvtxRange plan_range("render: plan (+ host read-back)");
       ESI_CUDA(h, launch_plan(h->d_chunk_first, h->d_chunk_n, (int)nc, h->d_tf, (int)F, t_cap,
                               h->allow_fast ? 1 : 0, h->d_info, h->d_n_active, st));
       ESI_CUDA(h, cudaMemcpyAsync(hna, h->d_n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       ESI_CUDA(h, cudaMemcpyAsync(hinfo.data(), h->d_info, nc * sizeof(ChunkInfo), cudaMemcpyDeviceToHost, st));
       ESI_CUDA(h, cudaStreamSynchronize(st));
-      ESI_CUDA(h, cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), st));
-      ESI_CUDA(h, cudaMemsetAsync(h->tile_ctr, 0, 4 * sizeof(uint32_t), st));   // K1 work counters (robust to an aborted launch)
     }
     const int n_act = std::max(1, *hna);
     const bool lazy = !h->prm.validate_on_push;
@@ -770,28 +797,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
         ESI_CUDA(h, cudaStreamWaitEvent(k1s, h->ev_h2d[bf], 0));
         k1_ev = h->stage_ev[bf];
       }
-      PartArgs pa{};
-      pa.ev = k1_ev;
-      pa.n = ch.n;
-      pa.index_base = index_base;
-      pa.prev_t = (c == 0) ? h->d_last_t : &chunks[c - 1].ptr[chunks[c - 1].n - 1].t_us;
-      pa.t_origin = h->prm.t_origin_us;
-      pa.last_frame_t = h->has_last_frame ? h->last_frame_t : INT64_MIN;
-      pa.t_min = h->has_last_frame ? std::max(h->prm.t_origin_us, h->last_frame_t + 1) : h->prm.t_origin_us;
-      pa.t_cap = t_cap;
-      pa.W = h->W;
-      pa.H = h->H;
-      pa.band_px = h->band_px;
-      pa.nb = h->nb;
-      pa.bm = h->bm;
-      pa.validate = h->prm.validate_on_push ? 0 : 1;
-      pa.rec = h->rec[bf];
-      pa.tile_ctr = h->tile_ctr + 2 * bf;
-      pa.meta = h->meta[bf];
-      pa.tile_t0 = h->tile_t0[bf];
-      pa.tile_wide = h->tile_wide[bf];
-      pa.wide_t = h->wide_t[bf];
-      pa.err = h->d_err;
+      PartArgs pa = k1_args(c, k1_ev, index_base);
       pa.gate_info = nosync ? h->d_info + c : nullptr;
       if (hinfo[c].active) {   // a chunk entirely after the last frame (only chunk 0 can be) is not partitioned
         TimedLaunch t1;
