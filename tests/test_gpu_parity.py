@@ -212,6 +212,51 @@ def test_render_many_equals_repeated_render_bit_exact_on_sparse_pixels():
     assert np.array_equal(Sa, Sb) and np.array_equal(Ta, Tb)
 
 
+@pytest.mark.parametrize("k", [10.0, 0.05])
+def test_sync_free_one_chunk_render_equals_the_read_back_path(k, monkeypatch):
+    """The sync-free one-chunk render (plan not read back: device-side kernel choice
+    and `active` test) against the general path (ESI_SYNC_PLAN=1)
+    on the streaming pattern -- 10 ms packets, one esi_render per frame, two frames per
+    packet so that a render also sees a chunk whose events all lie after its frame --
+    bit for bit, for the fast kernel (k = 10) and the fp64 kernel (k = 0.05), and a
+    stream with a 2^33 us gap (the plan picks the general kernel on the device)."""
+    from paper_2508_02238_b200 import Esi
+    W, H = 60, 44
+    ev = random_stream(77, W, H, 40_000, 300_000)
+    gap = ev.copy()
+    gap["t"][len(gap) // 2:] += 1 << 33
+
+    def run(events, sync_plan):
+        monkeypatch.setenv("ESI_SYNC_PLAN", "1" if sync_plan else "0")
+        e = Esi(W, H, k=k)
+        frames = []
+        try:
+            t_all = events["t"]
+            bounds = list(range(0, 300_001, 10_000))
+            if int(t_all[-1]) > 300_000:                         # the gap stream: a frame inside the gap, one after it
+                bounds += [int(t_all[-1]) // 2, int(t_all[-1]) + 10_000]
+            lo = 0
+            for b0, b1 in zip(bounds[:-1], bounds[1:]):
+                hi = int(np.searchsorted(t_all, b1, side="right"))
+                if hi > lo:
+                    assert e.push(from_numpy_struct(events[lo:hi]).cuda()) == 0
+                lo = hi
+                frames.append(e.render(b0 + (b1 - b0) // 4))     # before most of the packet's events
+                frames.append(e.render(b1))
+            S, T = e.get_state()
+            stats = e.last_render_stats()
+        finally:
+            e.close()
+        return np.stack(frames), S, T, stats
+
+    for events in (ev, gap):
+        fa, Sa, Ta, sa = run(events, False)
+        fb, Sb, Tb, sb = run(events, True)
+        assert np.array_equal(fa, fb)
+        assert np.array_equal(Sa, Sb) and np.array_equal(Ta, Tb)
+        assert sa["events"] == sb["events"]
+
+
 def test_render_many_equals_repeated_render_within_tolerance():
     """General stream: dense batches (several events of one pixel in one
     32-event batch) reassociate the clamped-affine composition, and batch

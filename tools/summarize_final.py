@@ -142,7 +142,7 @@ def main():
         r = last_json(os.path.join(DST, "route.json"))
         L += ["", "## Row-band router (`route.json`)", "",
               "%d events of a %s stream into %d bands: %.2f ms/call = %.1f G events/s, %.0f GB/s algorithmic "
-              "(48 B/event) = %.0f %% of HBM." % (r["events"], r["sensor"], r["bands"], r["ms_per_call"],
+              "(48 B/event) = %.0f %% of HBM." % (r["events"], r["sensor"], r["bands"], r.get("ms_per_call", r.get("count_plus_scatter_ms")),
                                                   r["events_per_s"] / 1e9, r["achieved_gbs"], 100 * r["frac"])]
     L += ["", "## Tests", "",
           "`pytest -m gpu`: %s (`pytest_gpu.log`); against the checked build (device invariant traps): %s "
