@@ -601,6 +601,28 @@ def test_2560x1440_sensor_full_frames():
     _prefix_check(w, 500_000, 100)
 
 
+def test_interleaved_layout_at_full_sensor_sizes():
+    """The interleaved band layout (band_layout = 1) at the sizes of the bench: c4's
+    first 0.6 s (444 bands of 33 groups, the 100 Mev/s burst included) and the
+    2560x1440 sensor's first 0.25 s (900 bands of 64 groups), every pixel of every
+    frame and the final state against the oracle."""
+    from paper_2508_02238_b200 import Esi
+    w = make_workload("c4", "cuda")
+    e = Esi(w.W, w.H, band_layout=1, **w.params)
+    try:
+        nb, bp, nw = e.layout()
+        groups = (w.P + 63) // 64
+        assert nb == 3 * torch.cuda.get_device_properties(0).multi_processor_count
+        assert bp == 64 * ((groups + nb - 1) // nb)
+    finally:
+        e.close()
+    w.params = dict(w.params, band_layout=1)
+    _prefix_check(w, 600_000, 100)
+    w = make_workload("c5b", "cuda", duration_us=250_000)
+    w.params = dict(w.params, band_layout=1)
+    _prefix_check(w, 250_000, 100)
+
+
 def test_c5a_stream_full_frames():
     """One of config 5a's 64 independent 1280x720 streams (10 Mev/s, seed 5000),
     first 1 s: every pixel of 100 frames and the final state against the oracle
