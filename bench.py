@@ -418,7 +418,7 @@ def stream_config(w, world, args, n_streams, n_distinct):
     return {"workload": wl, "sensor": f"{w.W}x{w.H}", "events_per_step_per_gpu": w.n * n_streams,
             "frames_per_step_per_gpu": len(w.t_frames) * n_streams, "esi_params": w.params,
             "validation": args.validation, "parallelism": par,
-            "band_layout": "interleaved" if os.environ.get("ESI_BAND_LAYOUT") == "1" else "contiguous (default)",
+            "band_layout": {"1": "interleaved", "2": "auto"}.get(os.environ.get("ESI_BAND_LAYOUT", ""), "contiguous (default)"),
             "l2": "inputs (16 B x events) and frames far larger than the 126 MB L2; no flush needed"}
 
 

@@ -108,6 +108,11 @@ typedef struct {
 
 #define ESI_BANDS_CONTIGUOUS 0
 #define ESI_BANDS_INTERLEAVED 1
+/* ESI_BANDS_AUTO: start contiguous; after a render whose busiest band held more than
+ * 3x the mean band's events (at least 100 k events), switch to the interleaved layout
+ * for the following renders (esi_reset returns to contiguous).  esi_layout reports
+ * the layout in use. */
+#define ESI_BANDS_AUTO 2
 
 typedef struct esi_handle esi_handle_t;
 

@@ -157,6 +157,11 @@ __global__ void __launch_bounds__(NW * 32) esi_integrate_wide_kernel(IntArgs a) 
     }
     if (threadIdx.x == 0) c.pre[n_tiles] = tot;
     n_b = (int)tot;
+    if (a.bstats && threadIdx.x == 0) {            // ESI_BANDS_AUTO: this band's share of the chunk
+      atomicMax(a.bstats, (unsigned long long)n_b);
+      atomicAdd(a.bstats + 1, (unsigned long long)n_b);
+      atomicAdd(a.bstats + 2, 1ull);
+    }
   }
   __syncthreads();
 

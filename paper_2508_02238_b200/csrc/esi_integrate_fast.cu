@@ -387,6 +387,11 @@ __global__ void __launch_bounds__(kNT, ESI_K2_MINB) esi_integrate_kernel(IntArgs
   }
   if (threadIdx.x == 0) *sm.nd = 0;
   const int n_b = active ? band_run_prefix<kNW>(a.meta + (int64_t)band * n_tiles, n_tiles, sm.pre, sm.mo, s_wsum) : 0;
+  if (a.bstats && active && threadIdx.x == 0) {   // ESI_BANDS_AUTO: this band's share of the chunk
+    atomicMax(a.bstats, (unsigned long long)n_b);
+    atomicAdd(a.bstats + 1, (unsigned long long)n_b);
+    atomicAdd(a.bstats + 2, 1ull);
+  }
   __syncthreads();
 
   int j = f_lo;

@@ -213,6 +213,9 @@ struct IntArgs {
   // sync-free single-chunk render: the host launches the fast and the general kernel without
   // reading the plan back; 1: run only if info->fast, 2: only if !info->fast, 0: run
   int32_t kind_gate;
+  // ESI_BANDS_AUTO: per render, {max, sum, count} of the bands' event counts over the chunks
+  // (one atomic update per CTA); null otherwise
+  unsigned long long* bstats;
 };
 
 struct ReadoutArgs {

@@ -64,7 +64,14 @@ struct esi_handle {
   int64_t P = 0;
   esi_params_t prm{};
   int band_px = 256, nb = 1;
-  BandMap bm{};              // pixel id <-> (band, local pixel)
+  BandMap bm{};              // pixel id <-> (band, local pixel), the layout in use
+  // both layouts of this sensor ([0] contiguous, [1] interleaved); ESI_BANDS_AUTO switches
+  // from [0] to [1] when a render's busiest band held > 3x the mean (bstats)
+  BandMap bm_of[2]{};
+  int nb_of[2] = {1, 1};
+  int layout_cur = 0;
+  bool layout_auto = false;
+  unsigned long long* d_bstats = nullptr;   // {max, sum, count} of band event counts of a render
   int64_t chunk_events = 0;
   int max_tiles = 0;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -280,7 +287,7 @@ int params_ok(const esi_params_t* p) {
   if (p->chunk_events < 0) return 0;
   if (p->decay_kind < 0 || p->decay_kind > 2 || p->decay_first < 0 || p->decay_first > 1) return 0;
   if (p->state_unclamped < 0 || p->state_unclamped > 1) return 0;
-  if (p->band_layout != ESI_BANDS_INTERLEAVED && p->band_layout != ESI_BANDS_CONTIGUOUS) return 0;
+  if (p->band_layout < ESI_BANDS_CONTIGUOUS || p->band_layout > ESI_BANDS_AUTO) return 0;
   return 1;
 }
 
@@ -409,12 +416,18 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
       nb = (ng + gpb - 1) / gpb;
     }
     gpb = (ng + nb - 1) / nb;                                  // no band larger than the round-robin needs
-    int interleave = prm.band_layout == ESI_BANDS_INTERLEAVED ? 1 : 0;
-    if (const char* e = getenv("ESI_BAND_LAYOUT")) interleave = atoi(e) == ESI_BANDS_INTERLEAVED ? 1 : 0;
-    if (!interleave) nb = (ng + gpb - 1) / gpb;                // contiguous runs of gpb groups: no empty band
+    int layout = prm.band_layout;
+    if (const char* e = getenv("ESI_BAND_LAYOUT")) layout = atoi(e);   // A/B override: 0, 1 or 2 (auto)
+    const int interleave = layout == ESI_BANDS_INTERLEAVED ? 1 : 0;
+    h->layout_auto = layout == ESI_BANDS_AUTO;
+    h->nb_of[1] = (int)nb;
+    h->nb_of[0] = (int)((ng + gpb - 1) / gpb);                 // contiguous runs of gpb groups: no empty band
+    h->bm_of[0] = make_band_map(h->nb_of[0], (int)gpb, 0);
+    h->bm_of[1] = make_band_map(h->nb_of[1], (int)gpb, 1);
     h->band_px = (int)(gpb * kGroup);
-    h->nb = (int)nb;
-    h->bm = make_band_map(h->nb, (int)gpb, interleave);
+    h->layout_cur = interleave;
+    h->nb = h->nb_of[interleave];
+    h->bm = h->bm_of[interleave];
   }
   int64_t ce = prm.chunk_events > 0 ? prm.chunk_events : (int64_t)8 << 20;
   ce = ((ce + kTile - 1) / kTile) * kTile;
@@ -433,7 +446,7 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   dalloc((void**)&h->dT, P * sizeof(int64_t));
   for (int b = 0; b < 2; ++b) {
     dalloc((void**)&h->rec[b], ce * sizeof(uint2));
-    dalloc((void**)&h->meta[b], (size_t)h->nb * h->max_tiles * sizeof(uint32_t));
+    dalloc((void**)&h->meta[b], (size_t)std::max(h->nb_of[0], h->nb_of[1]) * h->max_tiles * sizeof(uint32_t));
     dalloc((void**)&h->tile_t0[b], h->max_tiles * sizeof(int64_t));
     dalloc((void**)&h->tile_wide[b], h->max_tiles * sizeof(int32_t));
     dalloc((void**)&h->wide_t[b], ce * sizeof(int64_t));
@@ -451,6 +464,7 @@ int esi_create(int32_t width, int32_t height, const esi_params_t* params, esi_ha
   if (!rc && cudaMemset(h->tile_ctr, 0, 4 * sizeof(uint32_t)) != cudaSuccess) rc = ESI_ERR_CUDA;
   dalloc((void**)&h->d_last_t, sizeof(int64_t));
   dalloc((void**)&h->d_n_active, sizeof(int32_t));
+  dalloc((void**)&h->d_bstats, 3 * sizeof(unsigned long long));
   if (!rc) rc = ensure_pinned(h, 1 << 16);
   if (!rc) rc = esi_reset(h);
   // unclamped states (naive Eq. 2, complementary filter) are unbounded sums that can cancel:
@@ -501,7 +515,7 @@ void esi_destroy(esi_handle_t* h) {
   if (h->aux) cudaStreamSynchronize(h->aux);
   void* bufs[] = {h->dS, h->dT, h->rec[0], h->meta[0], h->tile_t0[0], h->tile_wide[0], h->wide_t[0],
                   h->rec[1], h->meta[1], h->tile_t0[1], h->tile_wide[1], h->wide_t[1], h->d_tf,
-                  (void*)h->d_chunk_first, h->d_chunk_n, h->d_info, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames, h->tile_ctr,
+                  (void*)h->d_chunk_first, h->d_chunk_n, h->d_info, h->d_cons, h->d_err, h->d_last_t, h->d_n_active, h->d_frames, h->tile_ctr, (void*)h->d_bstats,
                   h->dS_snap, h->dT_snap};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -534,6 +548,11 @@ int esi_reset(esi_handle_t* h) {
   h->sticky = ESI_OK;
   h->has_last_frame = false;
   h->last_frame_t = INT64_MIN;
+  if (h->layout_auto) {      // ESI_BANDS_AUTO starts every stream on contiguous bands
+    h->layout_cur = 0;
+    h->nb = h->nb_of[0];
+    h->bm = h->bm_of[0];
+  }
   ESI_CUDA(h, cudaMemsetAsync(h->dS, 0, h->P * sizeof(float), h->stream));
   ESI_CUDA(h, launch_fill_i64(h->dT, h->P, h->prm.t_origin_us, h->stream));
   ESI_CUDA(h, launch_fill_i64(h->d_last_t, 1, INT64_MIN, h->stream));
@@ -761,6 +780,8 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       ESI_CUDA(h, cudaStreamSynchronize(st));
     }
     const int n_act = std::max(1, *hna);
+    const bool watch = h->layout_auto && h->layout_cur == 0;   // ESI_BANDS_AUTO: watch the band balance
+    if (watch) ESI_CUDA(h, cudaMemsetAsync(h->d_bstats, 0, 3 * sizeof(unsigned long long), st));
     const bool lazy = !h->prm.validate_on_push;
     if (lazy) {   // lazy validation (fused in K1): keep the state so that a failing render leaves it untouched
       if (!h->dS_snap) {
@@ -832,6 +853,7 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       ia.mp = h->mp;
       ia.wp = h->wp;
       ia.gate = lazy ? h->d_err : nullptr;   // a K1 error so far: K2 exits (frames unspecified, S/T restored)
+      ia.bstats = watch ? h->d_bstats : nullptr;
       TimedLaunch t2;
       timed_begin(h, 1, &t2);
       if (nosync) {          // the plan decides on the device which of the two runs
@@ -866,6 +888,8 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
     if (rc) return rc;
     int64_t* hcons = (int64_t*)h->h_pin;
     unsigned long long* herr;
+    unsigned long long* hbs = (unsigned long long*)(h->h_pin + nc * 16 + h->segs.size() * sizeof(int64_t) + 64);
+    if (watch) ESI_CUDA(h, cudaMemcpyAsync(hbs, h->d_bstats, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (nosync) {   // one segment: {consumed, error word, kernel choice} in one kernel and one read-back
       ESI_CUDA(h, launch_finish1(h->segs[0].ptr, h->segs[0].n, t_cap, h->d_cons, h->d_last_t, h->d_err, h->d_info, st));
       h->st_launches += 1;
@@ -882,6 +906,12 @@ int esi_render_many(esi_handle_t* h, const int64_t* tf, size_t F, uint8_t* out) 
       ESI_CUDA(h, cudaMemcpyAsync(hcons, h->d_cons, (last_seg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
       ESI_CUDA(h, cudaMemcpyAsync(herr, h->d_err, sizeof(*herr), cudaMemcpyDeviceToHost, st));
       ESI_CUDA(h, cudaStreamSynchronize(st));
+    }
+    if (watch && *herr == kNoError && hbs[2] > 0 && hbs[1] >= 100000ull &&
+        hbs[0] * hbs[2] > 3ull * hbs[1]) {   // busiest band > 3x the mean: interleaved bands from the next render on
+      h->layout_cur = 1;
+      h->nb = h->nb_of[1];
+      h->bm = h->bm_of[1];
     }
     if (*herr != kNoError) {
       h->sticky = (int)(*herr & 0xff);

@@ -97,6 +97,42 @@ def test_band_layouts_against_oracle(layout):
         check(W, H, ev, tf, dict(DEF, k=0.05, band_layout=layout))          # fp64 kernel
 
 
+def test_auto_band_layout_switches_on_local_activity_and_keeps_parity():
+    """band_layout = 2 (ESI_BANDS_AUTO): a stream whose events all fall into a strip of the
+    sensor makes the busiest contiguous band hold far more than 3x the mean, so the handle
+    switches to interleaved bands after the first render -- frames of the renders before
+    and after the switch, and the final state, against the oracle; a stream spread over the
+    sensor stays on contiguous bands; esi_reset returns to contiguous."""
+    from paper_2508_02238_b200 import Esi
+    W, H, n = 320, 240, 400_000
+    rng = np.random.default_rng(5)
+    ev = random_stream(91, W, H, n, 400_000, cluster=False)
+    strip = ev.copy()
+    strip["y"] = (100 + rng.integers(0, 24, n)).astype(np.uint16)      # 10 % of the rows
+    tf = np.arange(1, 41, dtype=np.int64) * 10_000
+    for events, expect_switch in ((strip, True), (ev, False)):
+        f_ref, S_ref, T_ref = oracle_run(W, H, events, tf, DEF)
+        e = Esi(W, H, band_layout=2)
+        try:
+            nb0 = e.layout()[0]
+            assert e.push(from_numpy_struct(events).cuda()) == 0
+            frames = [e.render_many(tf[:10])]
+            nb1 = e.layout()[0]
+            frames += [e.render_many(tf[10:25]), e.render_many(tf[25:])]
+            S, T = e.get_state()
+            groups = (W * H + 63) // 64
+            if expect_switch:
+                assert nb1 == min(groups, 3 * torch.cuda.get_device_properties(0).multi_processor_count) and nb1 != nb0
+            else:
+                assert nb1 == nb0 and e.layout()[0] == nb0
+            e.reset()
+            assert e.layout()[0] == nb0
+        finally:
+            e.close()
+        assert_state_close(S, T, S_ref, T_ref)
+        assert_frames_close(np.concatenate(frames), f_ref)
+
+
 def test_band_layout_does_not_change_frames():
     """band_layout is a performance knob: on a stream whose pixels see at most one
     event per frame window per sub-batch path (sparse and chain paths, sequential fp32)

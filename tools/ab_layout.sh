@@ -10,7 +10,7 @@ import json; d=json.loads(open('gpurun_out/abl_$1_$2.json').read().strip().split
 print('%-8s layout %s  ms %.3f  %.1f G ev/s  K1 %.3f K2 %.3f  K2 launch %.1f us' % ('$1', '$2', d['ms_per_step'], d['value'] / 1e9, k['esi_partition_kernel'], k['esi_integrate_kernel'], 1e3*d['roofline']['mean_launch_ms']))" || tail -3 gpurun_out/abl_$1_$2.err
 }
 for rep in 1 2; do
-for L in 0 1; do
+for L in ${LAYOUTS:-0 1}; do
   run c4 $L ""
   run c4k $L "--fps 1000"
   run quarter $L "--roi 0.25,0.25,0.75,0.75"
